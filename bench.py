@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""KV restore benchmark (frames -> bf16 paged KV), B200.
+
+Workload (BASELINE.json configs[1]): Llama-3-8B-shaped K and V (32 layers -> 33
+padded = 11 layer triplets, 8 KV heads, head dim 128), 32,768 tokens, chunked
+into the reference's <=10,000-token containers (10000+10000+10000+2768) -> 88
+(K/V, triplet, chunk) units.  Frames are produced once on the GPU by our pack
+kernels from synthetic AR(1) bf16 KV (the reference generator's law); each step
+restores all 88 units into a vLLM-style paged cache (block size 16, shuffled
+block table) in one batched libkvf launch.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  value = KV restore GB/s (bf16 bytes delivered
+= 2 B x K+V elements of real layers / step time, device events, max over ranks).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODELS = {  # name -> (layers, kv heads, head dim)
+    "llama3-8b": (32, 8, 128),
+    "qwen2.5-7b": (28, 4, 128),
+    "llama3-70b": (80, 8, 128),
+}
+LAYOUTS = {  # name -> (a_h, b_h, a_d, b_d) as functions of (H, D)
+    "identity": lambda H, D: (1, H, 1, D),
+    "paper": lambda H, D: (H, 1, 1, D),
+}
+CHUNK = 10_000  # fk/container.py:29 DEFAULT_CHUNK_TOKENS
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama3-8b", choices=sorted(MODELS))
+    ap.add_argument("--tokens", type=int, default=32768)
+    ap.add_argument("--layout", default="identity", choices=sorted(LAYOUTS))
+    ap.add_argument("--res", default="R1080")
+    ap.add_argument("--page", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-units", type=int, default=2, help="sample units per CPU worker")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- workload
+def chunks_of(T):
+    out, t = [], 0
+    while t < T:
+        out.append((t, min(CHUNK, T - t)))
+        t += CHUNK
+    return out
+
+
+class Workload:
+    """Frames for every (K/V, triplet, chunk) unit + the paged destination cache."""
+
+    def __init__(self, args, device):
+        import torch
+        from paper_2602_09725_b200 import _dev, _lib, kvmodel as KV, layout as L
+        from paper_2602_09725_b200.restore import make_restore_unit
+
+        self.torch = torch
+        Lyr, H, D = MODELS[args.model]
+        self.Lyr, self.H, self.D, self.T = Lyr, H, D, args.tokens
+        self.gs = 128
+        lay = L.LayoutConfig(H, D, *LAYOUTS[args.layout](H, D))
+        self.lay = lay
+        trip = (Lyr + 2) // 3
+        bs = args.page
+        nblk = (self.T + bs - 1) // bs
+        g = torch.Generator(device="cpu")
+        g.manual_seed(1234)
+        self.table = torch.randperm(nblk + 64, generator=g)[:nblk].to(torch.int32).to(device)
+        self.pack_units, self.units, self.frames, self.scales = [], [], [], []
+        self.caches = []
+        self.elems = 0
+        for kv_i in range(2):  # K then V (seeds 0, 1 as in BASELINE.md)
+            kv = KV.gen_synthetic_kv(self.T, Lyr, H, D, 0.9, seed=kv_i, channel_smoothness=0.3,
+                                     dtype=torch.bfloat16).data
+            cache = torch.empty((Lyr, nblk + 64, bs, H, D), dtype=torch.bfloat16, device=device)
+            self.caches.append(cache)
+            for j in range(trip):
+                for (t0, tc) in chunks_of(self.T):
+                    plan = L.plan_inter_frame(tc, args.res, lay, 4)
+                    fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device=device)
+                    am = torch.empty((3, H * D // self.gs), dtype=torch.int32, device=device)
+                    sc = torch.empty((3, H * D // self.gs), dtype=torch.float32, device=device)
+                    src = _lib.kvf_paged()
+                    dst = _lib.kvf_paged()
+                    for p in range(3):
+                        l = 3 * j + p
+                        src.layer[p] = kv[:, l].data_ptr() if l < Lyr else None
+                        dst.layer[p] = cache[l].data_ptr() if l < Lyr else None
+                        if l < Lyr:
+                            self.elems += tc * H * D
+                    src.block_table = None
+                    src.block_size = 1
+                    src.dtype = _lib.KVF_BF16
+                    src.block_stride = src.slot_stride = Lyr * H * D
+                    src.head_stride = D
+                    src.token_base = t0
+                    dst.block_table = self.table.data_ptr()
+                    dst.block_size = bs
+                    dst.dtype = _lib.KVF_BF16
+                    dst.block_stride = bs * H * D
+                    dst.slot_stride = H * D
+                    dst.head_stride = D
+                    dst.token_base = t0
+                    pu = _lib.kvf_pack_unit()
+                    pu.src = src
+                    pu.plan = plan.to_c(self.gs)
+                    pu.absmax = am.data_ptr()
+                    pu.scales = sc.data_ptr()
+                    pu.frames = _dev.surface_of(fr)
+                    self.pack_units.append(pu)
+                    self.units.append(make_restore_unit(fr, plan, sc, dst, self.gs))
+                    self.frames.append(fr)
+                    self.scales.append(sc)
+                    self._keep = getattr(self, "_keep", []) + [am]
+            self.kv_src = getattr(self, "kv_src", []) + [kv]
+        self.frame_bytes = sum(f.numel() for f in self.frames)
+        self._pack_arr = (_lib.kvf_pack_unit * len(self.pack_units))(*self.pack_units)
+        self._restore_arr = (_lib.kvf_restore_unit * len(self.units))(*self.units)
+        self._lib, self._dev = _lib, _dev
+        self.n_launch_restore = (len(self.units) + _lib.KVF_MAX_UNITS - 1) // _lib.KVF_MAX_UNITS
+        self.n_launch_pack = 4 * self.n_launch_restore
+
+    def pack(self, stream):
+        self._lib.call("kvf_pack_batch", self._pack_arr, len(self.pack_units),
+                       self._dev.stream_ptr(stream))
+
+    def restore(self, stream):
+        self._lib.call("kvf_restore_batch", self._restore_arr, len(self.units),
+                       self._dev.stream_ptr(stream))
+
+
+def time_device(fn, stream, steps, warmup, torch, dist=None):
+    for _ in range(warmup):
+        fn(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    per = []
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with torch.cuda.stream(stream):
+        start.record(stream)
+        evs[0].record(stream)
+        for k in range(steps):
+            fn(stream)
+            evs[k + 1].record(stream)
+        stop.record(stream)
+    torch.cuda.synchronize()
+    total_ms = start.elapsed_time(stop)
+    per = [evs[k].elapsed_time(evs[k + 1]) for k in range(steps)]
+    return total_ms, per
+
+
+def e2e_restore(w, steps, torch):
+    """Same restore through the C ABI with HOST frames: per unit, a pinned H2D
+    copy on a copy stream overlapped with the previous unit's restore; one
+    2 KB D2H read of the last restored slot closes each step."""
+    from paper_2602_09725_b200 import _lib
+    dev = torch.device("cuda")
+    host = [torch.empty(f.shape, dtype=torch.uint8, pin_memory=True) for f in w.frames]
+    for h, f in zip(host, w.frames):
+        h.copy_(f)
+    nslot = 4
+    maxb = max(f.numel() for f in w.frames)
+    stage = [torch.empty(maxb, dtype=torch.uint8, device=dev) for _ in range(nslot)]
+    copy_s = torch.cuda.Stream()
+    comp_s = torch.cuda.Stream()
+    free_ev = [None] * nslot
+    out_host = torch.empty(w.H * w.D, dtype=torch.bfloat16, pin_memory=True)
+    units = []
+    for k, u in enumerate(w.units):
+        nu = _lib.kvf_restore_unit()
+        ctypes_copy(nu, u)
+        units.append(nu)
+
+    last = w.caches[1][w.Lyr - 1, int(w.table[0].item())][0].reshape(-1)
+
+    def step():
+        for k, u in enumerate(units):
+            s = k % nslot
+            buf = stage[s][: host[k].numel()].view(host[k].shape)
+            with torch.cuda.stream(copy_s):
+                if free_ev[s] is not None:
+                    copy_s.wait_event(free_ev[s])
+                buf.copy_(host[k], non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(copy_s)
+            comp_s.wait_event(ready)
+            u.frames.base = buf.data_ptr()
+            _lib.call("kvf_restore_batch", u, 1, w._dev.stream_ptr(comp_s))
+            ev = torch.cuda.Event()
+            ev.record(comp_s)
+            free_ev[s] = ev
+        with torch.cuda.stream(comp_s):
+            out_host.copy_(last, non_blocking=True)
+        comp_s.synchronize()
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    return ms, w.frame_bytes, out_host.numel() * 2
+
+
+def ctypes_copy(dst, src):
+    import ctypes
+    ctypes.memmove(ctypes.addressof(dst), ctypes.addressof(src), ctypes.sizeof(src))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh).get("hbm_gbs", 6650.0), "measured"
+    except OSError:
+        return 6650.0, "fallback"
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU restore path (oracle port) on host cores."""
+    if rank != 0:
+        return
+    from oracle import bench_cpu
+    Lyr, H, D = MODELS[args.model]
+    lay = (H, D) + LAYOUTS[args.layout](H, D)
+    times = []
+    for k in range(args.warmup + args.steps):
+        elems, wall, cores = bench_cpu.run("restore", units_per_worker=1, T=CHUNK, H=H, D=D,
+                                           res=args.res, lay=lay)
+        if k >= args.warmup:
+            times.append((elems, wall))
+    elems = sum(e for e, _ in times)
+    wall = sum(t for _, t in times)
+    gbs = 2.0 * elems / wall / 1e9
+    line = {
+        "metric": "KV restore GB/s (frames->bf16 paged KV), 32K ctx", "impl": "reference",
+        "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * wall / len(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16",
+        "data": "synthetic", "config": workload_config(args),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"{cores} processes x 1 unit of {CHUNK} tokens x 3 layers "
+                                   f"({args.model} shape, {args.layout}, {args.res}) per step"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    Lyr, H, D = MODELS[args.model]
+    return {"workload": f"{args.model}-shaped K+V, {args.tokens} tokens, {Lyr} layers "
+                        f"(+pad to x3), {H} KV heads, d={D}: frames -> bf16 paged KV restore",
+            "model_shape": args.model, "tokens": args.tokens, "layout": args.layout,
+            "resolution": args.res, "chunk_tokens": CHUNK, "group_size": 128, "F": 4,
+            "block_size": args.page, "parallelism": f"dp{args.gpus} (units sharded, no collective)",
+            "l2": "inputs larger than L2 (2.1 GB frames + 4.3 GB output per step)"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    d = dist if world > 1 else None
+
+    w = Workload(args, dev)
+    stream = torch.cuda.Stream()
+    # pack (secondary): frames for the restore steps come from here
+    pack_ms, pack_per = time_device(w.pack, stream, max(3, args.steps // 2), args.warmup, torch, d)
+    pack_ms /= max(3, args.steps // 2)
+    with ClockSampler(local) as clk:
+        total_ms, per = time_device(w.restore, stream, args.steps, args.warmup, torch, d)
+    ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms, pack_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, pack_ms = t.tolist()
+    elems_total = w.elems * world
+    value = 2.0 * elems_total / (ms * 1e-3) / 1e9
+    peak, peak_kind = load_peaks()
+    achieved = 3.0 * w.elems / (ms * 1e-3) / 1e9  # per GPU, algorithmic bytes
+    pack_ach = 3.0 * w.elems / (pack_ms * 1e-3) / 1e9
+
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h = e2e_restore(w, max(3, args.steps // 4), torch)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e = {"value": round(2.0 * elems_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(e2e_ms, 3),
+               "path": "pinned host frames -> H2D (copy stream) overlapped with per-unit "
+                       "kvf_restore_batch (compute stream) -> 2 KB D2H"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        from oracle import bench_cpu
+        Lyr, H, D = MODELS[args.model]
+        lay = (H, D) + LAYOUTS[args.layout](H, D)
+        elems, wall, cores = bench_cpu.run("restore", units_per_worker=args.cpu_units, T=CHUNK,
+                                           H=H, D=D, res=args.res, lay=lay)
+        cpu = {"value": round(2.0 * elems / wall / 1e9, 4), "unit": "GB/s", "cores": cores,
+               "kind": "port",
+               "sample": f"{cores} processes x {args.cpu_units} units of {CHUNK} tokens x 3 "
+                         f"layers: oracle disassemble_frames + dequantize + bf16 + paged scatter"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "KV restore GB/s (frames->bf16 paged KV), 32K ctx",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16", "data": "synthetic",
+            "config": workload_config(args),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_kind": peak_kind,
+                         "kernel": "restore_fast_kernel (kvf_restore_batch)",
+                         "algorithmic_bytes_per_step": 3 * w.elems},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": w.n_launch_restore * args.steps,
+            "clocks": clocks,
+            "pack": {"ms_per_step": round(pack_ms, 4),
+                     "achieved_gbs": round(pack_ach, 1), "frac": round(pack_ach / peak, 4),
+                     "launches_per_step": w.n_launch_pack},
+            "step_ms_min_max": [round(min(per), 4), round(max(per), 4)],
+            "units": len(w.units), "elems_per_gpu": w.elems,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+/*
+ * kvf.h — C ABI of the B200 (sm_100a) KV-frame hot path.
+ *
+ * This library replaces the data-parallel hot path of the reference `framekv`
+ * package (KVFetcher, arXiv 2602.09725; reference at pkg/src/framekv/, cited
+ * below as fk/<file>:<line>):
+ *
+ *   pack    = quantize (fk/kvmodel.py:127-144) + slice_tokens/assemble_frames
+ *             (fk/layout.py:109-114, 234-258)
+ *   restore = restore_stream.on_frame (fk/fetchsim.py:335-358) + inverse_layout
+ *             (fk/layout.py:137-147) + PagedMemory.page_write
+ *             (fk/kvmodel.py:216-229), fused with dequantize (fk/kvmodel.py:147-152)
+ *   decode  = codec.decode_frames (fk/codec.py:155-211) with its range coder
+ *             (fk/rangecoder.py:146-189) and predictor (fk/codec.py:131-144)
+ *
+ * The reference has no FFI of its own: its boundary is the Python signatures
+ * listed above.  These entry points are what a ctypes binding of that Python API
+ * calls.
+ *
+ * Conventions
+ *   - The caller owns every buffer.  The library never allocates or frees device
+ *     memory; device pointers are plain CUDA device pointers.
+ *   - Every launch goes on the caller's stream (`stream` is a cudaStream_t passed
+ *     as void*; NULL = legacy default stream).  No call synchronises the device
+ *     except where documented.
+ *   - Errors return a kvf_status; the message is kept per thread and read with
+ *     kvf_last_error().  There is no other global mutable state.
+ *   - All element strides are in ELEMENTS of the tensor's dtype, byte strides are
+ *     named *_bytes.  Channel index c = h*D + d, contiguous in d.
+ */
+#ifndef KVF_H_
+#define KVF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVF_ABI_VERSION 1
+
+/* Maximum units per batched launch (descriptors travel as kernel parameters). */
+#define KVF_MAX_UNITS 128
+
+typedef enum kvf_status {
+  KVF_OK = 0,
+  KVF_EINVAL = 1,        /* bad argument / shape: the reference raises ValueError */
+  KVF_ECUDA = 2,         /* a CUDA runtime call failed */
+  KVF_EUNSUPPORTED = 3,  /* valid for the reference, not handled by this build */
+  KVF_EDECODE = 4        /* corrupt bitstream: the reference raises DecodeError */
+} kvf_status;
+
+typedef enum kvf_dtype {
+  KVF_BF16 = 0,
+  KVF_F16 = 1,
+  KVF_F32 = 2,
+  KVF_I8 = 3  /* int8 quantized codes (PagedMemory slot contents in the reference) */
+} kvf_dtype;
+
+/*
+ * Frame plan of one chunk at one resolution class.  Mirrors LayoutConfig
+ * (fk/layout.py:31-86) and FramePlan (fk/layout.py:157-201):
+ *   element (h, d), h = i_h*b_h + j_h, d = i_d*b_d + j_d, lands at tile row
+ *   i_h*a_d + i_d, tile column j_h*b_d + j_d; tile_h = a_h*a_d, tile_w = b_h*b_d.
+ *   Token i: g,o = divmod(i, F); seg,slot = divmod(g, tiles_per_frame);
+ *   frame = seg*F + o; tile (slot / grid_cols, slot % grid_cols).
+ * frame_h/frame_w/frame_count are derived; kvf_plan_init fills them.
+ */
+typedef struct kvf_plan {
+  int32_t T;               /* tokens in the chunk */
+  int32_t H, D;            /* KV heads, head dim (powers of two) */
+  int32_t a_h, b_h, a_d, b_d;
+  int32_t F;               /* group frames (GOP) */
+  int32_t tiles_per_frame, grid_rows, grid_cols;
+  int32_t frame_h, frame_w, frame_count;
+  int32_t group_size;      /* quantization group (contiguous channels) */
+} kvf_plan;
+
+/*
+ * A sequence of 3-plane 8-bit frames: sample (f, p, y, x) lives at
+ *   base + f*frame_stride + p*plane_stride + y*row_pitch + x.
+ * The reference layout [n, 3, frame_h, frame_w] has row_pitch = frame_w,
+ * plane_stride = frame_h*frame_w, frame_stride = 3*plane_stride.  A decoder
+ * surface with a padded pitch is described by the same struct.
+ */
+typedef struct kvf_surface {
+  uint8_t* base;
+  int64_t frame_stride;
+  int64_t plane_stride;
+  int64_t row_pitch;
+} kvf_surface;
+
+/*
+ * Three layers of a (paged) KV cache, one pointer per plane p of the triplet.
+ * Token t of layer p (t = token_base + chunk token index) is the channel vector
+ * at element offset
+ *     blk*block_stride + (t % block_size)*slot_stride + h*head_stride + d
+ * of layer[p], where blk = block_table ? block_table[t / block_size]
+ *                                      : t / block_size.
+ * This is PagedMemory (fk/kvmodel.py:195-229: page = t // page_size_tokens,
+ * slot = t % page_size_tokens) with the page dict replaced by a block table,
+ * i.e. vLLM's [num_blocks, block_size, H, D] (NHD) or [num_blocks, H,
+ * block_size, D] (HND) per-layer caches.  layer[p] == NULL marks a pad layer
+ * (fk/kvmodel.py:56-69): restore never writes it, pack reads it as zeros.
+ * A contiguous [T, L, H, D] KVCache is block_table = NULL, block_size = 1,
+ * block_stride = slot_stride = L*H*D, head_stride = D, layer[p] = base + l*H*D.
+ */
+typedef struct kvf_paged {
+  void* layer[3];
+  const int32_t* block_table;
+  int32_t block_size;
+  int32_t dtype;           /* kvf_dtype of the cache */
+  int64_t block_stride;
+  int64_t slot_stride;
+  int64_t head_stride;
+  int32_t token_base;
+  int32_t reserved_;
+} kvf_paged;
+
+/* One (K-or-V, layer triplet, token chunk) unit of a batched restore. */
+typedef struct kvf_restore_unit {
+  kvf_surface frames;
+  kvf_plan plan;
+  const float* scales;     /* device [3, H*D/group_size] fp32 (container scales) */
+  kvf_paged dst;
+  int32_t first_frame;     /* restore frames [first_frame, first_frame+n_frames) */
+  int32_t n_frames;
+} kvf_restore_unit;
+
+/* One unit of a batched pack. */
+typedef struct kvf_pack_unit {
+  kvf_paged src;           /* bf16/f16/f32 KV to quantize, or int8 codes */
+  kvf_plan plan;
+  uint32_t* absmax;        /* device [3, G] scratch, bit patterns of |x| maxima */
+  float* scales;           /* device [3, G] out (ignored for int8 sources) */
+  kvf_surface frames;      /* out: frame_count frames */
+} kvf_pack_unit;
+
+/* ---- housekeeping ------------------------------------------------------- */
+int32_t kvf_abi_version(void);
+const char* kvf_last_error(void);
+
+/* Validate the layout/plan fields and derive frame_h/frame_w/frame_count;
+ * mirrors the checks of LayoutConfig.__init__ (fk/layout.py:38-50),
+ * FramePlan.__init__ (fk/layout.py:166-193) and plan_inter_frame
+ * (fk/layout.py:224-228). */
+kvf_status kvf_plan_init(kvf_plan* plan);
+
+/* Byte size of the frame surface a plan needs in the reference layout. */
+int64_t kvf_plan_frame_bytes(const kvf_plan* plan);
+
+/* ---- restore (frames -> paged KV), the headline path -------------------- */
+
+/* Frame-wise restore of frames [first_frame, first_frame+n_frames) of one
+ * chunk: every valid tile slot (fk/layout.py:203-212) is un-tiled, re-centred
+ * (u8 - 128), dequantised with the chunk scales (fk/kvmodel.py:147-152, fp32
+ * product, then RNE to the cache dtype; int8 caches receive the codes as the
+ * reference PagedMemory does) and written to its paged slot.
+ * Replaces fk/fetchsim.py:347-355 (on_frame) for a decoded frame batch. */
+kvf_status kvf_restore(const kvf_surface* frames, int32_t first_frame,
+                       int32_t n_frames, const kvf_plan* plan,
+                       const float* scales, const kvf_paged* dst, void* stream);
+
+/* Same for up to n_units units (split into launches of KVF_MAX_UNITS).
+ * `units` is a HOST array; descriptors are passed by value to the kernel. */
+kvf_status kvf_restore_batch(const kvf_restore_unit* units, int32_t n_units,
+                             void* stream);
+
+/* ---- pack (KV -> frames) ------------------------------------------------ */
+
+/* Phase 1: per (plane, group) max |x| over all chunk tokens, accumulated with
+ * atomicMax into `absmax` (which must be zeroed by the caller or by
+ * kvf_pack_batch).  fk/kvmodel.py:138-139. */
+kvf_status kvf_pack_absmax(const kvf_paged* src, const kvf_plan* plan,
+                           uint32_t* absmax, void* stream);
+
+/* Phase 2: scale = fp32(fp64(max)/127) or 1 (fk/kvmodel.py:140), exact
+ * round-half-even quantisation and clip (fk/kvmodel.py:141-143), +128, tile
+ * permutation and frame placement with pad byte 128 (fk/layout.py:234-258).
+ * Writes `scales` [3, G] too.  For an int8 `src` the codes are placed as-is
+ * (assemble_frames) and absmax/scales are ignored. */
+kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan,
+                           const uint32_t* absmax, float* scales,
+                           const kvf_surface* frames, void* stream);
+
+/* Both phases for up to n_units units, zeroing each unit's absmax first. */
+kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
+                          void* stream);
+
+/* ---- whole-tensor quantize / dequantize (fk/kvmodel.py:127-152) -------- */
+
+/* x: contiguous [T, L, C] of dtype src_dtype (bf16/f16/f32); absmax: [L, G]
+ * u32 scratch (zeroed here); scales: [L, G] fp32 out; values: [T, L, C] int8. */
+kvf_status kvf_quantize(const void* x, int32_t src_dtype, int64_t T, int32_t L,
+                        int32_t C, int32_t group_size, uint32_t* absmax,
+                        float* scales, int8_t* values, void* stream);
+
+/* values [T, L, C] int8, scales [L, G] -> out [T, L, C] of out_dtype. */
+kvf_status kvf_dequantize(const int8_t* values, const float* scales, int64_t T,
+                          int32_t L, int32_t C, int32_t group_size, void* out,
+                          int32_t out_dtype, void* stream);
+
+/* ---- synthetic inputs ---------------------------------------------------- */
+
+/* In-place AR(1) scan along the middle axis of an fp32 [outer, len, inner]
+ * tensor: x[o,t,i] = s*x[o,t-1,i] + (1-s)*x[o,t,i] (the law of gen_synthetic_kv,
+ * fk/kvmodel.py:155-192; used to build perf inputs on the GPU). */
+kvf_status kvf_ar1_scan(float* x, int64_t outer, int64_t len, int64_t inner,
+                        float s, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVF_H_ */

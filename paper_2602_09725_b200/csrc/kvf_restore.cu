@@ -1,0 +1,308 @@
+// kvf_restore.cu — frames -> (dequantised) paged KV cache, sm_100a.
+//
+// Replaces, for a batch of decoded frames, the reference's frame-wise restore
+// callback fk/fetchsim.py:347-355 (frame_slots -> tile -> int16-128 -> int8 ->
+// inverse_layout -> PagedMemory.page_write, fk/layout.py:137-147,203-212 and
+// fk/kvmodel.py:216-229) fused with dequantize (fk/kvmodel.py:147-152).
+//
+// Work decomposition: one warp per (frame, tile slot, plane) "item" = one token
+// slot of one layer.  Each lane owns VPL 8-channel vectors of the slot; its tile
+// offsets are computed once per CTA (the layout is per unit), so the per-item
+// cost is the item decode (frame/slot/token/page) amortised over the warp.  A
+// vector is one 8-byte read of 8 u8 samples (contiguous because b_d % 8 == 0)
+// and one 16-byte bf16 store into the 2*C-byte contiguous slot.  Each warp keeps
+// IPW*VPL loads in flight before it converts and stores.
+//
+// Bound: HBM.  Algorithmic bytes per channel element: 1 (u8 read) + sizeof(out).
+#include <algorithm>
+#include <vector>
+
+#include "kvf_common.cuh"
+
+namespace kvf {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kIPW = 2;  // items per warp
+
+struct RestoreUnitDev {
+  kvf_surface fr;
+  Geom g;
+  const float* scales;
+  kvf_paged dst;
+  int32_t first_frame;
+  int32_t n_items;  // n_frames * tiles_per_frame * 3
+  int32_t G;        // groups per layer
+};
+
+struct RestoreParams {
+  int32_t n_units;
+  RestoreUnitDev u[KVF_MAX_UNITS];
+};
+
+struct ItemPos {
+  int p, f, slot, i;
+};
+
+__device__ __forceinline__ ItemPos decode_item(const RestoreUnitDev& U,
+                                               int64_t j) {
+  ItemPos r;
+  int q = (int)(j / 3);
+  r.p = (int)(j - (int64_t)q * 3);
+  int fl = q / U.g.tpf;
+  r.slot = q - fl * U.g.tpf;
+  r.f = U.first_frame + fl;
+  r.i = token_of(U.g, r.f, r.slot);
+  return r;
+}
+
+__device__ __forceinline__ const uint8_t* tile_origin(const RestoreUnitDev& U,
+                                                      const ItemPos& x) {
+  int tr = x.slot / U.g.grid_cols;
+  int tc = x.slot - tr * U.g.grid_cols;
+  return U.fr.base + (int64_t)x.f * U.fr.frame_stride +
+         (int64_t)x.p * U.fr.plane_stride +
+         (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w;
+}
+
+template <int OUT, int VPL>
+__global__ void __launch_bounds__(kThreads)
+    restore_fast_kernel(const __grid_constant__ RestoreParams P) {
+  const RestoreUnitDev& U = P.u[blockIdx.y];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t item0 = ((int64_t)blockIdx.x * kWarps + warp) * kIPW;
+  if (item0 >= U.n_items) return;
+
+  constexpr int ES = OUT == KVF_F32 ? 4 : (OUT == KVF_I8 ? 1 : 2);
+  int32_t in_off[VPL];
+  int32_t out_off[VPL];
+  int32_t gidx[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    int c = (lane + 32 * k) * 8;
+    in_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
+    out_off[k] = (int32_t)slot_channel_offset(U.g, c, U.dst.head_stride);
+    gidx[k] = c / U.g.group_size;
+  }
+
+  uint2 v[kIPW][VPL];
+  char* outp[kIPW];
+  int plane[kIPW];
+#pragma unroll
+  for (int it = 0; it < kIPW; ++it) {
+    outp[it] = nullptr;
+    plane[it] = 0;
+    int64_t j = item0 + it;
+    if (j < U.n_items) {
+      ItemPos x = decode_item(U, j);
+      void* layer = U.dst.layer[x.p];
+      if (x.i < U.g.T && layer != nullptr) {
+        const uint8_t* src = tile_origin(U, x);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) v[it][k] = ld_nc_v2(src + in_off[k]);
+        outp[it] = reinterpret_cast<char*>(layer) +
+                   paged_slot_offset(U.dst, x.i) * ES;
+        plane[it] = x.p;
+      }
+    }
+  }
+
+#pragma unroll
+  for (int it = 0; it < kIPW; ++it) {
+    if (outp[it] == nullptr) continue;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      char* dst = outp[it] + (int64_t)out_off[k] * ES;
+      if constexpr (OUT == KVF_I8) {
+        // int8 code = u8 sample - 128 = sample ^ 0x80 (fk/fetchsim.py:351).
+        st_v2(dst, make_uint2(v[it][k].x ^ 0x80808080u, v[it][k].y ^ 0x80808080u));
+      } else {
+        const float s = __ldg(U.scales + plane[it] * U.G + gidx[k]);
+        float q[8];
+        bytes8_to_float(v[it][k].x, v[it][k].y, q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) q[e] *= s;
+        if constexpr (OUT == KVF_F32) {
+          st_v4(dst, make_uint4(__float_as_uint(q[0]), __float_as_uint(q[1]),
+                                __float_as_uint(q[2]), __float_as_uint(q[3])));
+          st_v4(dst + 16, make_uint4(__float_as_uint(q[4]), __float_as_uint(q[5]),
+                                     __float_as_uint(q[6]), __float_as_uint(q[7])));
+        } else if constexpr (OUT == KVF_BF16) {
+          st_v4(dst, make_uint4(pack_bf16x2(q[0], q[1]), pack_bf16x2(q[2], q[3]),
+                                pack_bf16x2(q[4], q[5]), pack_bf16x2(q[6], q[7])));
+        } else {
+          st_v4(dst, make_uint4(pack_f16x2(q[0], q[1]), pack_f16x2(q[2], q[3]),
+                                pack_f16x2(q[4], q[5]), pack_f16x2(q[6], q[7])));
+        }
+      }
+    }
+  }
+}
+
+// One thread per (item, channel): any layout, group size, alignment.
+__global__ void __launch_bounds__(kThreads)
+    restore_generic_kernel(const __grid_constant__ RestoreParams P) {
+  const RestoreUnitDev& U = P.u[blockIdx.y];
+  int64_t x = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  int64_t j = x >> U.g.lg_C;
+  if (j >= U.n_items) return;
+  int c = (int)(x & (U.g.C - 1));
+  ItemPos pos = decode_item(U, j);
+  void* layer = U.dst.layer[pos.p];
+  if (pos.i >= U.g.T || layer == nullptr) return;
+  const uint8_t* src = tile_origin(U, pos) + tile_offset(U.g, c, U.fr.row_pitch);
+  int q = (int)*src - 128;
+  float val = 0.0f;
+  if (U.dst.dtype != KVF_I8)
+    val = (float)q * __ldg(U.scales + pos.p * U.G + c / U.g.group_size);
+  int64_t o = paged_slot_offset(U.dst, pos.i) +
+              slot_channel_offset(U.g, c, U.dst.head_stride);
+  store_from_float(layer, o, U.dst.dtype, val, q);
+}
+
+bool aligned(const void* p, int64_t a) {
+  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+}
+
+// 0 = generic, else VPL of the fast kernel.
+int restore_variant(const kvf_restore_unit& u) {
+  const kvf_plan& p = u.plan;
+  int64_t C = (int64_t)p.H * p.D;
+  if (C % 256 != 0) return 0;
+  int vpl = (int)(C / 256);
+  if (vpl != 1 && vpl != 2 && vpl != 4 && vpl != 8 && vpl != 16) return 0;
+  if (p.b_d % 8 != 0) return 0;
+  if (u.dst.dtype != KVF_I8 && p.group_size % 8 != 0) return 0;
+  if (!aligned(u.frames.base, 8) || u.frames.frame_stride % 8 ||
+      u.frames.plane_stride % 8 || u.frames.row_pitch % 8)
+    return 0;
+  int64_t es = (int64_t)dtype_size(u.dst.dtype);
+  int64_t va = u.dst.dtype == KVF_I8 ? 8 : 16;  // bytes per vector store
+  for (int l = 0; l < 3; ++l)
+    if (u.dst.layer[l] && !aligned(u.dst.layer[l], va)) return 0;
+  if ((u.dst.head_stride * es) % va || (u.dst.slot_stride * es) % va ||
+      (u.dst.block_stride * es) % va)
+    return 0;
+  return vpl;
+}
+
+kvf_status check_unit(const kvf_restore_unit& u) {
+  kvf_status st = check_plan(u.plan);
+  if (st != KVF_OK) return st;
+  if (u.first_frame < 0 || u.n_frames < 0 ||
+      (int64_t)u.first_frame + u.n_frames > u.plan.frame_count)
+    KVF_FAIL(KVF_EINVAL, "frame range [%d, %d) outside the plan's %d frames",
+             u.first_frame, u.first_frame + u.n_frames, u.plan.frame_count);
+  if (u.n_frames > 0 && u.frames.base == nullptr)
+    KVF_FAIL(KVF_EINVAL, "null frame surface");
+  if (u.frames.row_pitch < u.plan.frame_w)
+    KVF_FAIL(KVF_EINVAL, "row pitch %lld below frame width %d",
+             (long long)u.frames.row_pitch, u.plan.frame_w);
+  if (u.dst.dtype < KVF_BF16 || u.dst.dtype > KVF_I8)
+    KVF_FAIL(KVF_EINVAL, "bad destination dtype %d", u.dst.dtype);
+  if (u.dst.dtype != KVF_I8 && u.scales == nullptr)
+    KVF_FAIL(KVF_EINVAL, "dequantising restore needs scales");
+  if (u.dst.block_size < 1) KVF_FAIL(KVF_EINVAL, "block_size must be >= 1");
+  if (u.dst.token_base < 0) KVF_FAIL(KVF_EINVAL, "negative token_base");
+  return KVF_OK;
+}
+
+RestoreUnitDev to_dev(const kvf_restore_unit& u) {
+  RestoreUnitDev d;
+  d.fr = u.frames;
+  d.g = make_geom(u.plan);
+  d.scales = u.scales;
+  d.dst = u.dst;
+  d.first_frame = u.first_frame;
+  d.n_items = u.n_frames * u.plan.tiles_per_frame * 3;
+  d.G = (u.plan.H * u.plan.D) / u.plan.group_size;
+  return d;
+}
+
+template <int OUT>
+void launch_fast(int vpl, const RestoreParams& P, dim3 grid, cudaStream_t s) {
+  switch (vpl) {
+    case 1: restore_fast_kernel<OUT, 1><<<grid, kThreads, 0, s>>>(P); break;
+    case 2: restore_fast_kernel<OUT, 2><<<grid, kThreads, 0, s>>>(P); break;
+    case 4: restore_fast_kernel<OUT, 4><<<grid, kThreads, 0, s>>>(P); break;
+    case 8: restore_fast_kernel<OUT, 8><<<grid, kThreads, 0, s>>>(P); break;
+    case 16: restore_fast_kernel<OUT, 16><<<grid, kThreads, 0, s>>>(P); break;
+  }
+}
+
+// Launch one group of units that share (variant, dtype).
+kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
+                        int32_t dtype, cudaStream_t s) {
+  for (size_t at = 0; at < units.size(); at += KVF_MAX_UNITS) {
+    size_t n = std::min<size_t>(KVF_MAX_UNITS, units.size() - at);
+    RestoreParams P;
+    P.n_units = (int32_t)n;
+    int64_t max_work = 0;
+    for (size_t k = 0; k < n; ++k) {
+      P.u[k] = to_dev(units[at + k]);
+      int64_t w = vpl ? P.u[k].n_items : (int64_t)P.u[k].n_items * P.u[k].g.C;
+      max_work = std::max(max_work, w);
+    }
+    if (max_work == 0) continue;
+    int64_t per_cta = vpl ? (int64_t)kWarps * kIPW : kThreads;
+    int64_t gx = (max_work + per_cta - 1) / per_cta;
+    if (gx > 0x7FFFFFFF) KVF_FAIL(KVF_EUNSUPPORTED, "restore grid too large");
+    dim3 grid((unsigned)gx, (unsigned)n);
+    if (vpl == 0) {
+      restore_generic_kernel<<<grid, kThreads, 0, s>>>(P);
+    } else {
+      switch (dtype) {
+        case KVF_BF16: launch_fast<KVF_BF16>(vpl, P, grid, s); break;
+        case KVF_F16: launch_fast<KVF_F16>(vpl, P, grid, s); break;
+        case KVF_F32: launch_fast<KVF_F32>(vpl, P, grid, s); break;
+        case KVF_I8: launch_fast<KVF_I8>(vpl, P, grid, s); break;
+      }
+    }
+    KVF_CHECK_CUDA(cudaGetLastError());
+  }
+  return KVF_OK;
+}
+
+}  // namespace
+}  // namespace kvf
+
+using namespace kvf;
+
+extern "C" kvf_status kvf_restore_batch(const kvf_restore_unit* units,
+                                        int32_t n_units, void* stream) {
+  if (n_units < 0 || (n_units > 0 && units == nullptr))
+    KVF_FAIL(KVF_EINVAL, "bad unit array");
+  // Group by (variant, dtype) so each launch instantiates one kernel.
+  std::vector<kvf_restore_unit> groups[17][4];
+  for (int32_t k = 0; k < n_units; ++k) {
+    kvf_status st = check_unit(units[k]);
+    if (st != KVF_OK) return st;
+    if (units[k].n_frames == 0) continue;
+    groups[restore_variant(units[k])][units[k].dst.dtype].push_back(units[k]);
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int v = 0; v <= 16; ++v)
+    for (int dt = 0; dt < 4; ++dt)
+      if (!groups[v][dt].empty()) {
+        kvf_status st = launch_group(groups[v][dt], v, dt, s);
+        if (st != KVF_OK) return st;
+      }
+  return KVF_OK;
+}
+
+extern "C" kvf_status kvf_restore(const kvf_surface* frames, int32_t first_frame,
+                                  int32_t n_frames, const kvf_plan* plan,
+                                  const float* scales, const kvf_paged* dst,
+                                  void* stream) {
+  if (!frames || !plan || !dst) KVF_FAIL(KVF_EINVAL, "null argument");
+  kvf_restore_unit u;
+  u.frames = *frames;
+  u.plan = *plan;
+  u.scales = scales;
+  u.dst = *dst;
+  u.first_frame = first_frame;
+  u.n_frames = n_frames;
+  return kvf_restore_batch(&u, 1, stream);
+}

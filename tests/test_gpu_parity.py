@@ -1,0 +1,290 @@
+"""GPU parity of the libkvf kernels against the reference goldens and the CPU oracle.
+
+Bar: bit-exact int8 codes, scales, frame bytes, page/slot placement; dequantised
+values bit-identical to the oracle's fp32 dequantize rounded once (RNE) to the
+cache dtype, hence within scale/2 (+ half a bf16 ulp) of the original KV.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_09725_b200 import _lib, layout as L, kvmodel as KV  # noqa: E402
+from paper_2602_09725_b200.restore import make_restore_unit, restore_frames, restore_units  # noqa: E402
+
+
+def sha_t(t):
+    return ref.digest(t.detach().cpu().numpy())
+
+
+def np_bf16_from_f32(x):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16)
+
+
+# ----------------------------------------------------------------- quantize
+@pytest.mark.parametrize("k", range(len(cases.QUANT_CASES)))
+def test_quantize_bit_exact(golden, k):
+    c = golden["quantize"][k]
+    x = cases.quant_input(c)
+    src = np_bf16_from_f32(x) if c.get("bf16") else torch.from_numpy(x)
+    if c.get("bf16"):
+        assert np.array_equal(src.float().numpy(), x)  # bf16-representable input
+    q = KV.quantize(KV.KVCache(src.cuda()), c["group_size"])
+    assert sha_t(q.values) == c["values"]
+    assert sha_t(q.scales) == c["scales"]
+    deq = KV.dequantize(q, torch.float32)
+    assert sha_t(deq.data) == c["dequant"]
+    ref_deq = torch.from_numpy(ref.dequantize(*ref.quantize(x, c["group_size"]), c["group_size"]))
+    for dt in (torch.bfloat16, torch.float16):
+        got = KV.dequantize(q, dt).data.cpu()
+        assert torch.equal(got, ref_deq.to(dt))
+
+
+def test_quantize_fp16_source():
+    x = cases.quant_input(dict(kind="synthetic", T=50, L=3, H=8, D=128, s=0.9, seed=2, c=0.3))
+    x16 = torch.from_numpy(x).half()
+    v, s = ref.quantize(x16.float().numpy(), 128)
+    q = KV.quantize(KV.KVCache(x16.cuda()), 128)
+    assert np.array_equal(q.values.cpu().numpy(), v)
+    assert np.array_equal(q.scales.cpu().numpy(), s)
+
+
+# ------------------------------------------------------------------- frames
+def test_assemble_disassemble_bit_exact(golden):
+    for c in golden["frames"]:
+        t = cases.frame_tensors(c)
+        plan = L.plan_inter_frame(c["T"], c["res"], L.LayoutConfig(*c["layout"]), c["F"])
+        fr = L.assemble_frames(torch.from_numpy(t).cuda(), plan)
+        assert list(fr.shape) == c["shape"]
+        assert sha_t(fr) == c["frames"], c
+        back = L.disassemble_frames(fr, plan)
+        assert np.array_equal(back.cpu().numpy(), t)
+
+
+def _pack_unit(kv_dev, lay, res, T0, T, F, gs, frames, absmax, scales, triplet=0):
+    """kvf_pack_unit for tokens [T0, T0+T) of layers 3*triplet.. of [T, L, H, D]."""
+    H, D = lay[0], lay[1]
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), F)
+    u = _lib.kvf_pack_unit()
+    Lyr = kv_dev.shape[1]
+    for p in range(3):
+        l = 3 * triplet + p
+        u.src.layer[p] = kv_dev[:, l].data_ptr() if l < Lyr else None
+    u.src.block_table = None
+    u.src.block_size = 1
+    u.src.dtype = {torch.bfloat16: 0, torch.float16: 1, torch.float32: 2}[kv_dev.dtype]
+    u.src.block_stride = u.src.slot_stride = Lyr * H * D
+    u.src.head_stride = D
+    u.src.token_base = T0
+    u.plan = plan.to_c(gs)
+    u.absmax = absmax.data_ptr()
+    u.scales = scales.data_ptr()
+    from paper_2602_09725_b200 import _dev
+    u.frames = _dev.surface_of(frames)
+    return u, plan
+
+
+@pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
+                                 (8, 128, 2, 4, 16, 8), (4, 64, 1, 4, 64, 1)])
+@pytest.mark.parametrize("res", ["R240", "R640", "R1080"])
+def test_fused_pack_matches_oracle(lay, res):
+    H, D = lay[0], lay[1]
+    T, Lyr, gs = 700, 5, 128 if D >= 128 else 64
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, Lyr, H, D, 0.9, 3, 0.3))
+    kv = np_bf16_from_f32(x).cuda()
+    chunks = [(0, 400), (400, 300)]
+    units, outs = [], []
+    for trip in range(2):
+        for T0, Tc in chunks:
+            plan = L.plan_inter_frame(Tc, res, L.LayoutConfig(*lay), 4)
+            fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
+            am = torch.empty((3, H * D // gs), dtype=torch.int32, device="cuda")
+            sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
+            u, plan = _pack_unit(kv, lay, res, T0, Tc, 4, gs, fr, am, sc, trip)
+            units.append(u)
+            outs.append((trip, T0, Tc, plan, fr, sc))
+    arr = (_lib.kvf_pack_unit * len(units))(*units)
+    _lib.call("kvf_pack_batch", arr, len(units), None)
+    torch.cuda.synchronize()
+    xp = ref.pad_layers(x)
+    for trip, T0, Tc, plan, fr, sc in outs:
+        slab = xp[T0:T0 + Tc, 3 * trip:3 * trip + 3]
+        v, s = ref.quantize(slab, gs)
+        oplan = ref.Plan(Tc, res, *lay, F=4)
+        want = ref.assemble_frames(v.reshape(Tc, 3, H * D), oplan)
+        assert np.array_equal(sc.cpu().numpy(), s)
+        assert np.array_equal(fr.cpu().numpy(), want)
+
+
+# ------------------------------------------------------------------ restore
+def _oracle_chunk(T, lay, res, seed, gs=128, F=4):
+    H, D = lay[0], lay[1]
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, 3, H, D, 0.9, seed, 0.3))
+    v, s = ref.quantize(x, gs)
+    plan = ref.Plan(T, res, *lay, F=F)
+    frames = ref.assemble_frames(v.reshape(T, 3, H * D), plan)
+    return x, v, s, frames
+
+
+@pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
+                                 (8, 128, 2, 4, 16, 8), (8, 128, 1, 8, 128, 1),
+                                 (4, 8, 2, 2, 4, 2)])
+@pytest.mark.parametrize("dtype", [torch.int8, torch.bfloat16, torch.float16, torch.float32])
+def test_restore_paged_matches_oracle(lay, dtype):
+    H, D = lay[0], lay[1]
+    gs = min(128, H * D)
+    T, res = 333, "R480"
+    x, v, s, frames = _oracle_chunk(T, lay, res, seed=4, gs=gs)
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+    mem = KV.PagedMemory(16, dtype=dtype)
+    mem.begin_fetch()
+    # scatter the logical pages over a shuffled physical pool
+    mem._ensure_layers(6)
+    mem._ensure_blocks(64)
+    rng = np.random.default_rng(0)
+    mem._free = list(rng.permutation(mem._free))
+    n = restore_frames(torch.from_numpy(frames).cuda(), plan, mem, layer_base=3,
+                       token_base=37, scales=torch.from_numpy(s).cuda())
+    assert n == T
+    torch.cuda.synchronize()
+    deq = ref.dequantize(v, s, gs).reshape(T, 3, H * D)
+    for tok in range(T):
+        for p in range(3):
+            got = mem.read(37 + tok, 3 + p).cpu()
+            if dtype == torch.int8:
+                assert np.array_equal(got.numpy(), v[tok, p].reshape(-1))
+            else:
+                assert torch.equal(got, torch.from_numpy(deq[tok, p]).to(dtype))
+    assert mem.read(36, 3) is None and mem.read(37, 0) is None
+    assert mem.allocated_bytes == T * 3 * H * D * torch.empty((), dtype=dtype).element_size()
+    with pytest.raises(KV.ConflictError):
+        restore_frames(torch.from_numpy(frames).cuda(), plan, mem, 3, 37, torch.from_numpy(s).cuda())
+    mem.begin_fetch()
+    restore_frames(torch.from_numpy(frames).cuda(), plan, mem, 3, 37, torch.from_numpy(s).cuda())
+
+
+def test_restore_golden_slots(golden):
+    for c in golden["restore"]:
+        kv = c["kv"]
+        v, s = ref.quantize(cases.quant_input(kv), kv["group_size"])
+        oplan = ref.Plan(kv["T"], c["res"], *c["layout"], F=c["F"])
+        frames = ref.assemble_frames(v.reshape(kv["T"], 3, kv["H"] * kv["D"]), oplan)
+        plan = L.plan_inter_frame(kv["T"], c["res"], L.LayoutConfig(*c["layout"]), c["F"])
+        mem = KV.PagedMemory(c["page"], dtype=torch.int8)
+        mem.begin_fetch()
+        # frame-wise: one launch per frame, like the reference's on_frame
+        fr_dev = torch.from_numpy(frames).cuda()
+        for f in range(plan.frame_count):
+            restore_frames(fr_dev[f:f + 1], plan, mem, c["layer_base"], c["token_base"],
+                           first_frame=f, n_frames=1)
+        blob = b"".join(mem.read(t, l).cpu().numpy().tobytes()
+                        for t in range(c["token_base"], c["token_base"] + kv["T"])
+                        for l in range(c["layer_base"], c["layer_base"] + 3))
+        assert ref.digest(blob) == c["slots"]
+        assert mem.allocated_bytes == c["allocated_bytes"]
+
+
+def test_restore_pad_layers_untouched():
+    lay = (8, 128, 1, 8, 1, 128)
+    T = 100
+    x, v, s, frames = _oracle_chunk(T, lay, "R240", seed=1)
+    plan = L.plan_inter_frame(T, "R240", L.LayoutConfig(*lay), 4)
+    mem = KV.PagedMemory(16, dtype=torch.bfloat16, H=8, D=128, num_blocks=16, num_layers=33)
+    for t in mem.layers:
+        t.fill_(7.0)
+    mem.begin_fetch()
+    restore_frames(torch.from_numpy(frames).cuda(), plan, mem, layer_base=30, token_base=0,
+                   scales=torch.from_numpy(s).cuda(), real_layers=32)
+    assert mem.read(0, 32) is None
+    assert torch.all(mem.layers[32] == 7.0)
+    assert mem.read(5, 31) is not None
+
+
+def test_restore_batch_mixed_units_and_layouts():
+    """Many units in one batched call: fast + generic kernels, HND layout, partial
+    frame ranges, different token bases — all against the oracle."""
+    from paper_2602_09725_b200 import _dev
+    specs = [((8, 128, 1, 8, 1, 128), "R1080", 500, 0, None),
+             ((8, 128, 8, 1, 1, 128), "R240", 257, 5, 3),
+             ((8, 128, 2, 4, 16, 8), "R640", 90, 0, None),
+             ((4, 8, 2, 2, 4, 2), "R240", 41, 2, 2),
+             ((8, 128, 1, 8, 128, 1), "R480", 77, 0, None)] * 12
+    units, checks = [], []
+    for k, (lay, res, T, f0, nf) in enumerate(specs):
+        H, D = lay[0], lay[1]
+        gs = min(128, H * D)
+        x, v, s, frames = _oracle_chunk(T, lay, res, seed=k, gs=gs)
+        plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+        nf = plan.frame_count - f0 if nf is None else nf
+        bs = 16
+        nblk = (T + bs - 1) // bs + 1
+        # HND per-layer cache [blocks, H, bs, D] for odd k, NHD otherwise
+        outs = [torch.zeros((nblk, H, bs, D) if k % 2 else (nblk, bs, H, D),
+                            dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+        table = torch.from_numpy(np.random.default_rng(k).permutation(nblk).astype(np.int32)).cuda()
+        dst = _lib.kvf_paged()
+        for p in range(3):
+            dst.layer[p] = outs[p].data_ptr()
+        dst.block_table = table.data_ptr()
+        dst.block_size = bs
+        dst.dtype = _lib.KVF_BF16
+        dst.block_stride = bs * H * D
+        dst.slot_stride = D if k % 2 else H * D
+        dst.head_stride = bs * D if k % 2 else D
+        dst.token_base = 0
+        fr = torch.from_numpy(frames).cuda()
+        sc = torch.from_numpy(s).cuda()
+        units.append(make_restore_unit(fr, plan, sc, dst, gs, f0, nf))
+        checks.append((lay, T, v, s, gs, plan, f0, nf, outs, table, fr, sc))
+    restore_units(units)
+    torch.cuda.synchronize()
+    for lay, T, v, s, gs, plan, f0, nf, outs, table, fr, sc in checks:
+        H, D = lay[0], lay[1]
+        deq = torch.from_numpy(ref.dequantize(v, s, gs)).to(torch.bfloat16)
+        toks = plan.tokens_in_frames(f0, nf)
+        tbl = table.cpu().numpy()
+        hnd = outs[0].shape[1] == H and outs[0].shape[2] == 16 and H != 16
+        for p in range(3):
+            o = outs[p].cpu()
+            written = torch.zeros(o.shape[:1] + (16,), dtype=torch.bool)
+            for t in toks:
+                blk, off = tbl[t // 16], t % 16
+                got = o[blk, :, off] if hnd else o[blk, off]
+                assert torch.equal(got.reshape(-1), deq[t, p].reshape(-1))
+                written[blk, off] = True
+            untouched = o[~written] if not hnd else o.permute(0, 2, 1, 3)[~written]
+            assert torch.all(untouched == 0)
+
+
+# ----------------------------------------------------------- large property
+def test_c2_unit_round_trip_property():
+    """Full-size unit (10,000 tokens, Llama-3-8B triplet, R1080): pack -> restore
+    reproduces quantize() codes exactly and dequantize() values bit-for-bit."""
+    from paper_2602_09725_b200 import _dev
+    T, H, D, gs = 10000, 8, 128, 128
+    kv = KV.gen_synthetic_kv(T, 3, H, D, 0.9, seed=0, channel_smoothness=0.3,
+                             dtype=torch.bfloat16)
+    q = KV.quantize(kv, gs)
+    lay = (8, 128, 1, 8, 1, 128)
+    plan = L.plan_inter_frame(T, "R1080", L.LayoutConfig(*lay), 4)
+    fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
+    am = torch.empty((3, 8), dtype=torch.int32, device="cuda")
+    sc = torch.empty((3, 8), dtype=torch.float32, device="cuda")
+    u, _ = _pack_unit(kv.data, lay, "R1080", 0, T, 4, gs, fr, am, sc)
+    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
+    assert torch.equal(sc, q.scales)
+    assert torch.equal(fr, L.assemble_frames(q.values.reshape(T, 3, H * D), plan))
+    for dt in (torch.int8, torch.bfloat16):
+        mem = KV.PagedMemory(16, dtype=dt)
+        mem.begin_fetch()
+        restore_frames(fr, plan, mem, 0, 0, scales=sc)
+        cache = torch.stack([mem.layers[p][torch.as_tensor(
+            [mem.pages[t // 16] for t in range(0, T, 16)], device="cuda")].reshape(-1, H, D)[:T]
+            for p in range(3)], dim=1)
+        want = q.values if dt == torch.int8 else KV.dequantize(q, torch.bfloat16).data
+        assert torch.equal(cache, want)
