@@ -41,10 +41,44 @@ inline bool is_pow2(int64_t v) { return v >= 1 && (v & (v - 1)) == 0; }
 kvf_status check_plan(const kvf_plan& p);
 size_t dtype_size(int32_t dt);
 
+// Division by a runtime-constant divisor d >= 1 for dividends n < 2^31:
+// q = umulhi(n, m) >> s with m = ceil(2^(31+ceil(log2 d)) / d), s = ceil(log2 d)-1
+// (the multiply-high scheme of Granlund & Montgomery); d == 1 passes through.
+struct FastDiv {
+  uint32_t m;
+  int32_t s;
+  int32_t d;
+};
+
+inline FastDiv make_fastdiv(int32_t d) {
+  FastDiv f;
+  f.d = d;
+  if (d <= 1) {
+    f.m = 0;
+    f.s = 0;
+    return f;
+  }
+  int l = ilog2(d);
+  uint64_t p = 31 + l;
+  f.m = (uint32_t)(((uint64_t(1) << p) + d - 1) / d);
+  f.s = l - 1;
+  return f;
+}
+
+__host__ __device__ __forceinline__ int32_t fdiv(const FastDiv& f, int32_t n) {
+#ifdef __CUDA_ARCH__
+  return f.d == 1 ? n : (int32_t)(__umulhi((uint32_t)n, f.m) >> f.s);
+#else
+  return n / f.d;
+#endif
+}
+
 // Plan fields the kernels need, with log2 of the power-of-two extents.
 struct Geom {
   int32_t T, F, tpf, grid_cols, tile_h, tile_w, frame_count;
   int32_t lg_D, lg_bh, lg_bd, a_d, C, lg_C, group_size;
+  int32_t lg_gs;  // group_size divides the power-of-two channel count: a power of two
+  FastDiv div_tpf, div_F, div_cols;
 };
 
 inline Geom make_geom(const kvf_plan& p) {
@@ -63,6 +97,10 @@ inline Geom make_geom(const kvf_plan& p) {
   g.C = p.H * p.D;
   g.lg_C = ilog2(g.C);
   g.group_size = p.group_size;
+  g.lg_gs = ilog2(p.group_size);
+  g.div_tpf = make_fastdiv(p.tiles_per_frame);
+  g.div_F = make_fastdiv(p.F);
+  g.div_cols = make_fastdiv(p.grid_cols);
   return g;
 }
 
@@ -92,7 +130,7 @@ __device__ __forceinline__ int64_t slot_channel_offset(const Geom& g, int c,
 // Token placement (fk/layout.py:195-201) in the frame-major direction used by
 // frame_slots (fk/layout.py:203-212): frame f, slot -> chunk token index.
 __device__ __forceinline__ int token_of(const Geom& g, int f, int slot) {
-  int seg = f / g.F;
+  int seg = fdiv(g.div_F, f);
   int o = f - seg * g.F;
   return (seg * g.tpf + slot) * g.F + o;
 }
@@ -105,6 +143,17 @@ __device__ __forceinline__ int64_t paged_slot_offset(const kvf_paged& pg, int i)
   int64_t blk = pg.block_table ? (int64_t)__ldg(pg.block_table + blk_logical)
                                : blk_logical;
   return blk * pg.block_stride + in_blk * pg.slot_stride;
+}
+
+// Same with a fast divisor for the block size (t < 2^31).
+__device__ __forceinline__ int64_t paged_slot_offset_fd(const kvf_paged& pg,
+                                                        const FastDiv& bs, int i) {
+  int32_t t = pg.token_base + i;
+  int32_t blk_logical = fdiv(bs, t);
+  int32_t in_blk = t - blk_logical * pg.block_size;
+  int64_t blk = pg.block_table ? (int64_t)__ldg(pg.block_table + blk_logical)
+                               : (int64_t)blk_logical;
+  return blk * pg.block_stride + (int64_t)in_blk * pg.slot_stride;
 }
 
 // Quantization scale of one group from its |x| maximum (fk/kvmodel.py:139-140):
@@ -179,6 +228,75 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
                : "l"(p));
   return v;
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ---- mbarrier + TMA bulk copy (cp.async.bulk) helpers -------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
+                                             uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+// L2 eviction-priority policies (createpolicy) and loads/stores that carry them.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_nc_v4_pol(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_v2_pol(void* p, uint2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(v.x),
+               "r"(v.y), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)

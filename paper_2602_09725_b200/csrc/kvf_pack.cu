@@ -1,52 +1,46 @@
-// kvf_pack.cu — (paged) KV -> quantised 3-plane frames, sm_100a.
+// kvf_pack.cu — (paged) KV -> quantised 3-plane frames, sm_100a: entry points,
+// the phase-split kernels and the L2-reuse fused fallback.
 //
 // Replaces quantize (fk/kvmodel.py:127-144) + slice_tokens (fk/layout.py:109-114)
-// + assemble_frames (fk/layout.py:234-258) for one (layer triplet, token chunk)
-// unit, in three launches per batch:
-//   1. absmax  — per (plane, group) max |x| over the chunk's tokens
-//                (fk/kvmodel.py:138-139): warp-per-token, lanes keep running
-//                maxima of the 16-bit |x| patterns (order-preserving for
-//                non-negative bf16/fp16), xor-shuffle reduce inside the group,
-//                shared atomicMax across warps, one global atomicMax per CTA.
-//   2. scales  — fp32(fp64(max)/127) or 1.0 (fk/kvmodel.py:140).
-//   3. frames  — warp per (frame, tile slot) of one plane (grid.z = plane):
-//                16-byte source loads, exact half-even rounding + clip
-//                (fk/kvmodel.py:141-142), +128, 8-byte stores at the tile
-//                position; slots past T and pad layers get PAD_BYTE 128
-//                (fk/layout.py:231, 251-253).
-// An int8 source skips 1-2 and places the codes (assemble_frames).
+// + assemble_frames (fk/layout.py:234-258) for (layer triplet, token chunk) units.
+//
+// kvf_pack_batch picks, per group of units:
+//   1. pack_coop_kernel (kvf_pack_coop.cu): one cooperative launch, source
+//      staged once in SMEM by TMA bulk copies — 3 B of HBM traffic per element;
+//   2. pack_fused_kernel (below): persistent queue of absmax / quantise tiles
+//      with per-plane dependency counters; the second source read is served
+//      from L2 (evict_last on the first read) — for shapes that do not fit 1;
+//   3. the phase-split kernels (absmax -> scales -> frames), also used by the
+//      single-phase entry points and for int8 sources (assemble_frames).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
-#include "kvf_common.cuh"
+#include "kvf_pack_common.cuh"
 
 namespace kvf {
+
+kvf_status launch_pack_coop(const std::vector<kvf_pack_unit>& units, int32_t dtype,
+                            cudaStream_t s, bool* launched);
+
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kIPW = 2;          // frame items per warp
-constexpr int kTokPerWarp = 8;   // absmax tokens per warp
-
-struct PackUnitDev {
-  kvf_paged src;
-  Geom g;
-  uint32_t* absmax;
-  float* scales;
-  kvf_surface fr;
-  int32_t n_items;  // frame_count * tiles_per_frame (per plane)
-  int32_t G;
-};
+constexpr int kThreads = kPackThreads;
+constexpr int kWarps = kPackWarps;
+constexpr int kIPW = 8;         // frame items per warp (phase-split frames kernel)
+constexpr int kTokPerWarp = 8;  // absmax tokens per warp (phase-split absmax kernel)
 
 struct PackParams {
   int32_t n_units;
-  PackUnitDev u[KVF_MAX_UNITS];
+  PackUnitDev u[kMaxPackUnits];
 };
 
 // ------------------------------------------------------------------ phase 0/2
 __global__ void zero_absmax_kernel(const __grid_constant__ PackParams P) {
   const PackUnitDev& U = P.u[blockIdx.y];
-  for (int k = threadIdx.x; k < 3 * U.G; k += blockDim.x) U.absmax[k] = 0u;
+  for (int k = threadIdx.x; k < U.n_scratch; k += blockDim.x) U.absmax[k] = 0u;
 }
 
 __global__ void finalize_scales_kernel(const __grid_constant__ PackParams P) {
@@ -55,35 +49,22 @@ __global__ void finalize_scales_kernel(const __grid_constant__ PackParams P) {
     U.scales[k] = scale_from_absmax_bits(U.absmax[k]);
 }
 
-// -------------------------------------------------------------------- phase 1
-template <int SRC>
-__device__ __forceinline__ uint32_t vec_absmax_bits(const char* p) {
-  if constexpr (SRC == KVF_F32) {
-    uint4 a = ld_nc_v4(p), b = ld_nc_v4(p + 16);
-    uint32_t m = max(max(a.x & 0x7FFFFFFFu, a.y & 0x7FFFFFFFu),
-                     max(a.z & 0x7FFFFFFFu, a.w & 0x7FFFFFFFu));
-    m = max(m, max(max(b.x & 0x7FFFFFFFu, b.y & 0x7FFFFFFFu),
-                   max(b.z & 0x7FFFFFFFu, b.w & 0x7FFFFFFFu)));
-    return m;
-  } else {
-    uint4 a = ld_nc_v4(p);
-    uint32_t w0 = a.x & 0x7FFF7FFFu, w1 = a.y & 0x7FFF7FFFu;
-    uint32_t w2 = a.z & 0x7FFF7FFFu, w3 = a.w & 0x7FFF7FFFu;
-    uint32_t hi = max(max(w0, w1), max(w2, w3)) & 0xFFFF0000u;  // high halves
-    uint32_t lo = max(max(w0 & 0xFFFFu, w1 & 0xFFFFu), max(w2 & 0xFFFFu, w3 & 0xFFFFu));
-    return max(hi >> 16, lo);
+// Warp-group reduction of per-lane maxima into s_max[group] (lanes lane+32k of
+// one group are gs/8 consecutive lanes when gs <= 256, else the whole warp).
+template <int SRC, int VPL>
+__device__ __forceinline__ void reduce_groups(const uint32_t (&m)[VPL], int group_size,
+                                              uint32_t* s_max) {
+  const int lane = threadIdx.x & 31;
+  const int lpg = group_size >> 3;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    uint32_t v = absmax_to_f32_bits<SRC>(m[k]);
+    for (int o = 1; o < 32 && o < lpg; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((lane & (min(lpg, 32) - 1)) == 0 && v) atomicMax(&s_max[(lane + 32 * k) / lpg], v);
   }
 }
 
-// 16-bit |x| pattern (or f32 bits) -> f32 bits of |x|.
-template <int SRC>
-__device__ __forceinline__ uint32_t absmax_to_f32_bits(uint32_t m) {
-  if constexpr (SRC == KVF_BF16) return m << 16;
-  if constexpr (SRC == KVF_F16)
-    return __float_as_uint(__half2float(__ushort_as_half((unsigned short)m)));
-  return m;
-}
-
+// -------------------------------------------------------------------- phase 1
 template <int SRC, int VPL>
 __global__ void __launch_bounds__(kThreads)
     absmax_fast_kernel(const __grid_constant__ PackParams P) {
@@ -96,35 +77,23 @@ __global__ void __launch_bounds__(kThreads)
   if (blockIdx.x * kWarps * kTokPerWarp >= U.g.T || layer == nullptr) return;
   for (int k = threadIdx.x; k < U.G; k += kThreads) s_max[k] = 0u;
   __syncthreads();
-
   constexpr int ES = SRC == KVF_F32 ? 4 : 2;
   int32_t off[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k)
-    off[k] = (int32_t)slot_channel_offset(U.g, (lane + 32 * k) * 8, U.src.head_stride) * ES;
   uint32_t m[VPL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) m[k] = 0u;
-
+  for (int k = 0; k < VPL; ++k) {
+    off[k] = (int32_t)slot_channel_offset(U.g, (lane + 32 * k) * 8, U.src.head_stride) * ES;
+    m[k] = 0u;
+  }
 #pragma unroll 2
   for (int t = 0; t < kTokPerWarp; ++t) {
     int i = tok0 + t;
     if (i >= U.g.T) break;
-    const char* slot = layer + paged_slot_offset(U.src, i) * ES;
+    const char* slot = layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) m[k] = max(m[k], vec_absmax_bits<SRC>(slot + off[k]));
   }
-
-  // Lanes (lane + 32k) of one group are gs/8 consecutive lanes (gs <= 256) or
-  // the whole warp over several k (gs > 256).
-  const int lpg = U.g.group_size >> 3;  // lanes per group (vectors per group)
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    uint32_t v = absmax_to_f32_bits<SRC>(m[k]);
-    for (int o = 1; o < 32 && o < lpg; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    int vec = lane + 32 * k;
-    if ((lane & (min(lpg, 32) - 1)) == 0 && v) atomicMax(&s_max[vec / lpg], v);
-  }
+  reduce_groups<SRC, VPL>(m, U.g.group_size, s_max);
   __syncthreads();
   for (int k = threadIdx.x; k < U.G; k += kThreads)
     if (s_max[k]) atomicMax(&U.absmax[p * U.G + k], s_max[k]);
@@ -154,48 +123,18 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // -------------------------------------------------------------------- phase 3
-template <int SRC>
-__device__ __forceinline__ void load_vec8(const char* p, float (&x)[8]) {
-  if constexpr (SRC == KVF_F32) {
-    uint4 a = ld_nc_v4(p), b = ld_nc_v4(p + 16);
-    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y);
-    x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
-    x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y);
-    x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
-  } else {
-    uint4 a = ld_nc_v4(p);
-    uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if constexpr (SRC == KVF_BF16) {
-        x[2 * k] = __uint_as_float(w[k] << 16);
-        x[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
-      } else {
-        __half2 h = *reinterpret_cast<__half2*>(&w[k]);
-        float2 f = __half22float2(h);
-        x[2 * k] = f.x;
-        x[2 * k + 1] = f.y;
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ uint32_t pack_codes4(int a, int b, int c, int d) {
-  return (uint32_t)((a + 128) & 0xFF) | ((uint32_t)((b + 128) & 0xFF) << 8) |
-         ((uint32_t)((c + 128) & 0xFF) << 16) | ((uint32_t)((d + 128) & 0xFF) << 24);
-}
-
-template <int SRC, int VPL>
+// kRange: scales may come from a caller's absmax (kvf_pack_frames), so |x/s|
+// is not bounded by 127 and the clip must be checked.
+template <int SRC, int VPL, bool kRange>
 __global__ void __launch_bounds__(kThreads)
     pack_fast_kernel(const __grid_constant__ PackParams P) {
   const PackUnitDev& U = P.u[blockIdx.y];
   const int p = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item0 = ((int64_t)blockIdx.x * kWarps + warp) * kIPW;
+  const int item0 = (blockIdx.x * kWarps + warp) * kIPW;
   if (item0 >= U.n_items) return;
   constexpr int ES = SRC == KVF_F32 ? 4 : (SRC == KVF_I8 ? 1 : 2);
   const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
-
   int32_t in_off[VPL], tile_off[VPL];
   float s[VPL], inv[VPL];
 #pragma unroll
@@ -204,53 +143,90 @@ __global__ void __launch_bounds__(kThreads)
     in_off[k] = (int32_t)slot_channel_offset(U.g, c, U.src.head_stride) * ES;
     tile_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
     if constexpr (SRC != KVF_I8) {
-      s[k] = U.scales[p * U.G + c / U.g.group_size];
+      s[k] = U.scales[p * U.G + (c >> U.g.lg_gs)];
       inv[k] = __frcp_rn(s[k]);
     }
   }
-
+  uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
+  // Item q -> (tile origin in the plane, source slot or null for a pad tile).
+  auto locate = [&](int q, uint8_t*& dst, const char*& srcp) {
+    const int f = fdiv(U.g.div_tpf, q);
+    const int slot = q - f * U.g.tpf;
+    const int i = token_of(U.g, f, slot);
+    const int tr = fdiv(U.g.div_cols, slot);
+    const int tc = slot - tr * U.g.grid_cols;
+    dst = plane_base + (int64_t)f * U.fr.frame_stride +
+          (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w;
+    srcp = (i < U.g.T && layer != nullptr)
+               ? layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES
+               : nullptr;
+  };
+  if constexpr (SRC == KVF_I8 || VPL > 4) {
+    for (int it = 0; it < kIPW; ++it) {
+      const int q = item0 + it;
+      if (q >= U.n_items) break;
+      uint8_t* dst;
+      const char* slotp;
+      locate(q, dst, slotp);
+      if (slotp == nullptr) {
 #pragma unroll
-  for (int it = 0; it < kIPW; ++it) {
-    int j = (int)(item0 + it);
-    if (j >= U.n_items) break;
-    int f = j / U.g.tpf;
-    int slot = j - f * U.g.tpf;
-    int i = token_of(U.g, f, slot);
-    int tr = slot / U.g.grid_cols;
-    int tc = slot - tr * U.g.grid_cols;
-    uint8_t* dst = U.fr.base + (int64_t)f * U.fr.frame_stride +
-                   (int64_t)p * U.fr.plane_stride +
-                   (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w;
-    if (i >= U.g.T || layer == nullptr) {
+        for (int k = 0; k < VPL; ++k)
+          st_v2(dst + tile_off[k], make_uint2(0x80808080u, 0x80808080u));
+        continue;
+      }
+      if constexpr (SRC == KVF_I8) {
+        uint2 v[VPL];
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) st_v2(dst + tile_off[k], make_uint2(0x80808080u, 0x80808080u));
-      continue;
-    }
-    const char* slotp = layer + paged_slot_offset(U.src, i) * ES;
-    if constexpr (SRC == KVF_I8) {
-      uint2 v[VPL];
+        for (int k = 0; k < VPL; ++k) v[k] = ld_nc_v2(slotp + in_off[k]);
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) v[k] = ld_nc_v2(slotp + in_off[k]);
+        for (int k = 0; k < VPL; ++k)
+          st_v2(dst + tile_off[k], make_uint2(v[k].x ^ 0x80808080u, v[k].y ^ 0x80808080u));
+      } else {
 #pragma unroll
-      for (int k = 0; k < VPL; ++k)
-        st_v2(dst + tile_off[k], make_uint2(v[k].x ^ 0x80808080u, v[k].y ^ 0x80808080u));
-    } else {
-      // At most 4 vectors (32 values) live at once to bound register use.
-      constexpr int KB = VPL < 4 ? VPL : 4;
+        for (int k0 = 0; k0 < VPL; k0 += 4) {  // at most 32 live values per lane
+          float x[4][8];
 #pragma unroll
-      for (int k0 = 0; k0 < VPL; k0 += KB) {
-        float x[KB][8];
+          for (int k = 0; k < 4; ++k) load_vec8<SRC>(slotp + in_off[k0 + k], x[k]);
 #pragma unroll
-        for (int k = 0; k < KB; ++k) load_vec8<SRC>(slotp + in_off[k0 + k], x[k]);
-#pragma unroll
-        for (int k = 0; k < KB; ++k) {
-          int q[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) q[e] = quantize_exact(x[k][e], s[k0 + k], inv[k0 + k]);
-          st_v2(dst + tile_off[k0 + k], make_uint2(pack_codes4(q[0], q[1], q[2], q[3]),
-                                                   pack_codes4(q[4], q[5], q[6], q[7])));
+          for (int k = 0; k < 4; ++k)
+            st_v2(dst + tile_off[k0 + k], quantize8<kRange>(x[k], s[k0 + k], inv[k0 + k]));
         }
       }
+    }
+  } else {
+    // Software pipeline: the loads of item it+1 are in flight while item it is
+    // quantised and stored.
+    Raw8<SRC> cur[VPL], nxt[VPL];
+    uint8_t* dst_cur = nullptr;
+    const char* src_cur = nullptr;
+    const int n_it = min(kIPW, U.n_items - item0);
+    locate(item0, dst_cur, src_cur);
+    if (src_cur)
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) cur[k] = load_raw8<SRC>(src_cur + in_off[k]);
+    for (int it = 0; it < n_it; ++it) {
+      uint8_t* dst_nxt = nullptr;
+      const char* src_nxt = nullptr;
+      if (it + 1 < n_it) {
+        locate(item0 + it + 1, dst_nxt, src_nxt);
+        if (src_nxt)
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) nxt[k] = load_raw8<SRC>(src_nxt + in_off[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        uint2 out = make_uint2(0x80808080u, 0x80808080u);
+        if (src_cur) {
+          float x[8];
+          raw8_to_float<SRC>(cur[k], x);
+          out = quantize8<kRange>(x, s[k], inv[k]);
+        }
+        st_v2(dst_cur + tile_off[k], out);
+      }
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) cur[k] = nxt[k];
+      dst_cur = dst_nxt;
+      src_cur = src_nxt;
     }
   }
 }
@@ -268,8 +244,7 @@ __global__ void __launch_bounds__(kThreads)
   int i = token_of(U.g, f, slot);
   int tr = slot / U.g.grid_cols;
   int tc = slot - tr * U.g.grid_cols;
-  uint8_t* dst = U.fr.base + (int64_t)f * U.fr.frame_stride +
-                 (int64_t)p * U.fr.plane_stride +
+  uint8_t* dst = U.fr.base + (int64_t)f * U.fr.frame_stride + (int64_t)p * U.fr.plane_stride +
                  (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w +
                  tile_offset(U.g, c, U.fr.row_pitch);
   const void* layer = U.src.layer[p];
@@ -288,9 +263,156 @@ __global__ void __launch_bounds__(kThreads)
   *dst = (uint8_t)(q + 128);
 }
 
-bool aligned(const void* p, int64_t a) {
-  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+// ------------------------------------------------- L2-reuse fused fallback
+//
+// Single queue of tiles ordered A(0) | A(1) | A(2) Q(0) | A(3) Q(1) | ... where
+// A(s) computes the |x| maxima of sub-unit s = (unit, plane) and Q(s) quantises
+// it.  CTAs take tiles from an atomic counter; a Q tile of s waits for the
+// counter of s to reach its A-tile count.  A tiles of s precede its Q tiles in
+// the queue and a CTA waits only between tiles, so every awaited tile is held
+// by a running CTA (no deadlock, no co-residency requirement).  First reads
+// carry evict_last, re-reads and frame stores evict_first, so Q(s) re-reads
+// its slab from L2.
+constexpr int kATokPerWarp = 16;
+constexpr int kATok = kWarps * kATokPerWarp;  // tokens per A tile
+constexpr int kQPerWarp = 4;
+constexpr int kQItems = kWarps * kQPerWarp;   // frame slots per Q tile
+constexpr int kMaxFusedUnits = 96;
+constexpr int kMaxSub = 3 * kMaxFusedUnits;
+constexpr int kLag = 2;  // Q(s) sits kLag segments after A(s)
+
+struct FusedParams {
+  int32_t n_units;
+  int32_t n_sub;
+  int32_t total_tiles;
+  uint32_t* queue;
+  PackUnitDev u[kMaxFusedUnits];
+  int32_t seg_begin[kMaxSub + kLag + 1];  // segment s = A(s) + Q(s - kLag)
+  uint16_t n_a[kMaxSub];
+};
+
+template <int SRC, int VPL>
+__device__ __forceinline__ void fused_a_tile(const PackUnitDev& U, int p, int tile,
+                                             uint32_t* s_max) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
+  constexpr int ES = SRC == KVF_F32 ? 4 : 2;
+  for (int k = threadIdx.x; k < U.G; k += kThreads) s_max[k] = 0u;
+  __syncthreads();
+  int32_t off[VPL];
+  uint32_t m[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    off[k] = (int32_t)slot_channel_offset(U.g, (lane + 32 * k) * 8, U.src.head_stride) * ES;
+    m[k] = 0u;
+  }
+  const int tok0 = tile * kATok + warp * kATokPerWarp;
+  const WithPolicy keep{l2_policy_evict_last()};
+#pragma unroll 4
+  for (int t = 0; t < kATokPerWarp; ++t) {
+    int i = tok0 + t;
+    if (i >= U.g.T) break;
+    const char* slot = layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) m[k] = max(m[k], vec_absmax_bits<SRC>(slot + off[k], keep));
+  }
+  reduce_groups<SRC, VPL>(m, U.g.group_size, s_max);
+  __syncthreads();
+  for (int k = threadIdx.x; k < U.G; k += kThreads) {
+    if (s_max[k]) atomicMax(&U.absmax[p * U.G + k], s_max[k]);
+    __threadfence();  // each writer makes its reduction visible before the barrier
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(&U.done[p], 1u);
 }
+
+template <int SRC, int VPL>
+__device__ __forceinline__ void fused_q_tile(const PackUnitDev& U, int p, int tile, int n_a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0 && n_a > 0) {
+    long long spins = 0;
+    while (ld_acquire_u32(&U.done[p]) < (uint32_t)n_a) {
+      __nanosleep(128);
+      if (++spins == (1ll << 28)) __trap();  // broken schedule: fail hard, never hang
+    }
+  }
+  __syncthreads();
+  const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
+  constexpr int ES = SRC == KVF_F32 ? 4 : 2;
+  if (tile == 0)  // one CTA per sub-unit publishes the scales (fk/kvmodel.py:140)
+    for (int k = threadIdx.x; k < U.G; k += kThreads)
+      U.scales[p * U.G + k] = scale_from_absmax_bits(__ldcg(&U.absmax[p * U.G + k]));
+  int32_t in_off[VPL], tile_off[VPL];
+  float s[VPL], inv[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    int c = (lane + 32 * k) * 8;
+    in_off[k] = (int32_t)slot_channel_offset(U.g, c, U.src.head_stride) * ES;
+    tile_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
+    s[k] = scale_from_absmax_bits(__ldcg(&U.absmax[p * U.G + (c >> U.g.lg_gs)]));
+    inv[k] = __frcp_rn(s[k]);
+  }
+  uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
+  const int q0 = tile * kQItems + warp * kQPerWarp;
+  const uint64_t drop = l2_policy_evict_first();
+  const WithPolicy last_use{drop};
+#pragma unroll 1
+  for (int it = 0; it < kQPerWarp; ++it) {
+    const int q = q0 + it;
+    if (q >= U.n_items) break;
+    const int f = fdiv(U.g.div_tpf, q);
+    const int slot = q - f * U.g.tpf;
+    const int i = token_of(U.g, f, slot);
+    const int tr = fdiv(U.g.div_cols, slot);
+    const int tc = slot - tr * U.g.grid_cols;
+    uint8_t* dst = plane_base + (int64_t)f * U.fr.frame_stride +
+                   (int64_t)tr * U.g.tile_h * U.fr.row_pitch + tc * U.g.tile_w;
+    if (i >= U.g.T || layer == nullptr) {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        st_v2_pol(dst + tile_off[k], make_uint2(0x80808080u, 0x80808080u), drop);
+      continue;
+    }
+    const char* slotp = layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES;
+    constexpr int KB = VPL < 4 ? VPL : 4;
+#pragma unroll
+    for (int k0 = 0; k0 < VPL; k0 += KB) {
+      float x[KB][8];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) load_vec8<SRC>(slotp + in_off[k0 + k], x[k], last_use);
+#pragma unroll
+      for (int k = 0; k < KB; ++k)
+        st_v2_pol(dst + tile_off[k0 + k], quantize8<false>(x[k], s[k0 + k], inv[k0 + k]), drop);
+    }
+  }
+}
+
+template <int SRC, int VPL>
+__global__ void __launch_bounds__(kThreads, 3)
+    pack_fused_kernel(const __grid_constant__ FusedParams P) {
+  extern __shared__ uint32_t s_max[];
+  __shared__ int s_tile;
+  int seg = 0;  // cursor into seg_begin (tiles arrive in increasing order per CTA)
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(P.queue, 1u);
+    __syncthreads();
+    const int t = s_tile;
+    if (t >= P.total_tiles) break;
+    while (P.seg_begin[seg + 1] <= t) ++seg;
+    const int local = t - P.seg_begin[seg];
+    const int na = seg < P.n_sub ? (int)P.n_a[seg] : 0;
+    if (local < na) {
+      fused_a_tile<SRC, VPL>(P.u[seg / 3], seg % 3, local, s_max);
+    } else {
+      const int s = seg - kLag;
+      fused_q_tile<SRC, VPL>(P.u[s / 3], s % 3, local - na, (int)P.n_a[s]);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- host
+bool aligned(const void* p, int64_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 int pack_variant(const kvf_pack_unit& u) {
   const kvf_plan& p = u.plan;
@@ -300,8 +422,8 @@ int pack_variant(const kvf_pack_unit& u) {
   if (vpl != 1 && vpl != 2 && vpl != 4 && vpl != 8 && vpl != 16) return 0;
   if (p.b_d % 8 != 0) return 0;
   if (u.src.dtype != KVF_I8 && p.group_size % 8 != 0) return 0;
-  if (!aligned(u.frames.base, 8) || u.frames.frame_stride % 8 ||
-      u.frames.plane_stride % 8 || u.frames.row_pitch % 8)
+  if (!aligned(u.frames.base, 8) || u.frames.frame_stride % 8 || u.frames.plane_stride % 8 ||
+      u.frames.row_pitch % 8)
     return 0;
   int64_t es = (int64_t)dtype_size(u.src.dtype);
   int64_t va = u.src.dtype == KVF_I8 ? 8 : 16;
@@ -317,32 +439,20 @@ kvf_status check_unit(const kvf_pack_unit& u) {
   kvf_status st = check_plan(u.plan);
   if (st != KVF_OK) return st;
   if (u.frames.base == nullptr) KVF_FAIL(KVF_EINVAL, "null frame surface");
-  if (u.frames.row_pitch < u.plan.frame_w)
-    KVF_FAIL(KVF_EINVAL, "row pitch below frame width");
+  if (u.frames.row_pitch < u.plan.frame_w) KVF_FAIL(KVF_EINVAL, "row pitch below frame width");
   if (u.src.dtype < KVF_BF16 || u.src.dtype > KVF_I8)
     KVF_FAIL(KVF_EINVAL, "bad source dtype %d", u.src.dtype);
   if (u.src.dtype != KVF_I8 && (u.absmax == nullptr || u.scales == nullptr))
     KVF_FAIL(KVF_EINVAL, "quantising pack needs absmax scratch and scales");
   if (u.src.block_size < 1) KVF_FAIL(KVF_EINVAL, "block_size must be >= 1");
   if (u.src.token_base < 0) KVF_FAIL(KVF_EINVAL, "negative token_base");
+  if ((int64_t)u.src.token_base + u.plan.T >= (int64_t(1) << 31))
+    KVF_FAIL(KVF_EUNSUPPORTED, "token index beyond 2^31");
   return KVF_OK;
 }
 
-PackUnitDev to_dev(const kvf_pack_unit& u) {
-  PackUnitDev d;
-  d.src = u.src;
-  d.g = make_geom(u.plan);
-  d.absmax = u.absmax;
-  d.scales = u.scales;
-  d.fr = u.frames;
-  d.n_items = u.plan.frame_count * u.plan.tiles_per_frame;
-  d.G = (u.plan.H * u.plan.D) / u.plan.group_size;
-  return d;
-}
-
 template <int SRC>
-void launch_absmax_fast(int vpl, const PackParams& P, dim3 grid, size_t smem,
-                        cudaStream_t s) {
+void launch_absmax_fast(int vpl, const PackParams& P, dim3 grid, size_t smem, cudaStream_t s) {
   switch (vpl) {
     case 1: absmax_fast_kernel<SRC, 1><<<grid, kThreads, smem, s>>>(P); break;
     case 2: absmax_fast_kernel<SRC, 2><<<grid, kThreads, smem, s>>>(P); break;
@@ -352,86 +462,184 @@ void launch_absmax_fast(int vpl, const PackParams& P, dim3 grid, size_t smem,
   }
 }
 
-template <int SRC>
-void launch_pack_fast(int vpl, const PackParams& P, dim3 grid, cudaStream_t s) {
+template <int SRC, bool kRange>
+void launch_pack_fast_r(int vpl, const PackParams& P, dim3 grid, cudaStream_t s) {
   switch (vpl) {
-    case 1: pack_fast_kernel<SRC, 1><<<grid, kThreads, 0, s>>>(P); break;
-    case 2: pack_fast_kernel<SRC, 2><<<grid, kThreads, 0, s>>>(P); break;
-    case 4: pack_fast_kernel<SRC, 4><<<grid, kThreads, 0, s>>>(P); break;
-    case 8: pack_fast_kernel<SRC, 8><<<grid, kThreads, 0, s>>>(P); break;
-    case 16: pack_fast_kernel<SRC, 16><<<grid, kThreads, 0, s>>>(P); break;
+    case 1: pack_fast_kernel<SRC, 1, kRange><<<grid, kThreads, 0, s>>>(P); break;
+    case 2: pack_fast_kernel<SRC, 2, kRange><<<grid, kThreads, 0, s>>>(P); break;
+    case 4: pack_fast_kernel<SRC, 4, kRange><<<grid, kThreads, 0, s>>>(P); break;
+    case 8: pack_fast_kernel<SRC, 8, kRange><<<grid, kThreads, 0, s>>>(P); break;
+    case 16: pack_fast_kernel<SRC, 16, kRange><<<grid, kThreads, 0, s>>>(P); break;
   }
 }
 
-// phases: bit 0 = zero absmax, bit 1 = absmax, bit 2 = scales, bit 3 = frames.
-kvf_status launch_group(const std::vector<kvf_pack_unit>& units, int vpl,
-                        int32_t dtype, int phases, cudaStream_t s) {
-  for (size_t at = 0; at < units.size(); at += KVF_MAX_UNITS) {
-    size_t n = std::min<size_t>(KVF_MAX_UNITS, units.size() - at);
-    PackParams P;
-    P.n_units = (int32_t)n;
+// trusted: the scales were derived in this call from the same source's maxima.
+template <int SRC>
+void launch_pack_fast(int vpl, const PackParams& P, dim3 grid, cudaStream_t s, bool trusted) {
+  if (trusted || SRC == KVF_I8)
+    launch_pack_fast_r<SRC, false>(vpl, P, grid, s);
+  else
+    launch_pack_fast_r<SRC, true>(vpl, P, grid, s);
+}
+
+PackParams* make_params(const std::vector<kvf_pack_unit>& units, size_t at, size_t n) {
+  PackParams* P = new PackParams();
+  P->n_units = (int32_t)n;
+  for (size_t k = 0; k < n; ++k) P->u[k] = make_pack_unit_dev(units[at + k]);
+  return P;
+}
+
+// phases: bit 0 = zero scratch, bit 1 = absmax, bit 2 = scales, bit 3 = frames.
+kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+                         int phases, cudaStream_t s) {
+  for (size_t at = 0; at < units.size(); at += kMaxPackUnits) {
+    size_t n = std::min<size_t>(kMaxPackUnits, units.size() - at);
+    PackParams* P = make_params(units, at, n);
     int64_t max_items = 0, max_T = 0, max_G = 1, max_C = 1;
     for (size_t k = 0; k < n; ++k) {
-      P.u[k] = to_dev(units[at + k]);
-      max_items = std::max<int64_t>(max_items, P.u[k].n_items);
-      max_T = std::max<int64_t>(max_T, P.u[k].g.T);
-      max_G = std::max<int64_t>(max_G, P.u[k].G);
-      max_C = std::max<int64_t>(max_C, P.u[k].g.C);
+      max_items = std::max<int64_t>(max_items, P->u[k].n_items);
+      max_T = std::max<int64_t>(max_T, P->u[k].g.T);
+      max_G = std::max<int64_t>(max_G, P->u[k].G);
+      max_C = std::max<int64_t>(max_C, P->u[k].g.C);
     }
     const bool quant = dtype != KVF_I8;
     size_t smem = (size_t)max_G * sizeof(uint32_t);
-    if (smem > 48 * 1024) KVF_FAIL(KVF_EUNSUPPORTED, "too many quantisation groups");
-    if (quant && (phases & 1)) {
-      zero_absmax_kernel<<<dim3(1, (unsigned)n), 256, 0, s>>>(P);
-      KVF_CHECK_CUDA(cudaGetLastError());
+    cudaError_t e = cudaSuccess;
+    if (smem > 48 * 1024) {
+      delete P;
+      KVF_FAIL(KVF_EUNSUPPORTED, "too many quantisation groups");
     }
+    if (quant && (phases & 1)) zero_absmax_kernel<<<dim3(1, (unsigned)n), 256, 0, s>>>(*P);
     if (quant && (phases & 2) && max_T > 0) {
       if (vpl) {
         int64_t per = (int64_t)kWarps * kTokPerWarp;
         dim3 grid((unsigned)((max_T + per - 1) / per), (unsigned)n, 3);
         switch (dtype) {
-          case KVF_BF16: launch_absmax_fast<KVF_BF16>(vpl, P, grid, smem, s); break;
-          case KVF_F16: launch_absmax_fast<KVF_F16>(vpl, P, grid, smem, s); break;
-          case KVF_F32: launch_absmax_fast<KVF_F32>(vpl, P, grid, smem, s); break;
+          case KVF_BF16: launch_absmax_fast<KVF_BF16>(vpl, *P, grid, smem, s); break;
+          case KVF_F16: launch_absmax_fast<KVF_F16>(vpl, *P, grid, smem, s); break;
+          case KVF_F32: launch_absmax_fast<KVF_F32>(vpl, *P, grid, smem, s); break;
         }
       } else {
         int64_t work = max_T * max_C;
         dim3 grid((unsigned)((work + kThreads - 1) / kThreads), (unsigned)n, 3);
-        absmax_generic_kernel<<<grid, kThreads, smem, s>>>(P);
+        absmax_generic_kernel<<<grid, kThreads, smem, s>>>(*P);
       }
-      KVF_CHECK_CUDA(cudaGetLastError());
     }
-    if (quant && (phases & 4)) {
-      finalize_scales_kernel<<<dim3(1, (unsigned)n), 256, 0, s>>>(P);
-      KVF_CHECK_CUDA(cudaGetLastError());
-    }
+    if (quant && (phases & 4)) finalize_scales_kernel<<<dim3(1, (unsigned)n), 256, 0, s>>>(*P);
     if ((phases & 8) && max_items > 0) {
       if (vpl) {
         int64_t per = (int64_t)kWarps * kIPW;
         dim3 grid((unsigned)((max_items + per - 1) / per), (unsigned)n, 3);
+        const bool trusted = (phases & 2) != 0;
         switch (dtype) {
-          case KVF_BF16: launch_pack_fast<KVF_BF16>(vpl, P, grid, s); break;
-          case KVF_F16: launch_pack_fast<KVF_F16>(vpl, P, grid, s); break;
-          case KVF_F32: launch_pack_fast<KVF_F32>(vpl, P, grid, s); break;
-          case KVF_I8: launch_pack_fast<KVF_I8>(vpl, P, grid, s); break;
+          case KVF_BF16: launch_pack_fast<KVF_BF16>(vpl, *P, grid, s, trusted); break;
+          case KVF_F16: launch_pack_fast<KVF_F16>(vpl, *P, grid, s, trusted); break;
+          case KVF_F32: launch_pack_fast<KVF_F32>(vpl, *P, grid, s, trusted); break;
+          case KVF_I8: launch_pack_fast<KVF_I8>(vpl, *P, grid, s, trusted); break;
         }
       } else {
         int64_t work = max_items * max_C;
-        if ((work + kThreads - 1) / kThreads > 0x7FFFFFFF)
+        if ((work + kThreads - 1) / kThreads > 0x7FFFFFFF) {
+          delete P;
           KVF_FAIL(KVF_EUNSUPPORTED, "pack grid too large");
+        }
         dim3 grid((unsigned)((work + kThreads - 1) / kThreads), (unsigned)n, 3);
-        pack_generic_kernel<<<grid, kThreads, 0, s>>>(P);
+        pack_generic_kernel<<<grid, kThreads, 0, s>>>(*P);
       }
-      KVF_CHECK_CUDA(cudaGetLastError());
+    }
+    e = cudaGetLastError();
+    delete P;
+    if (e != cudaSuccess) return cuda_status(e, "pack phase kernels");
+  }
+  return KVF_OK;
+}
+
+template <int SRC, int VPL>
+kvf_status launch_fused_t(const FusedParams& P, size_t smem, cudaStream_t s) {
+  int dev = 0, sms = 0, occ = 0;
+  KVF_CHECK_CUDA(cudaGetDevice(&dev));
+  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  KVF_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &occ, pack_fused_kernel<SRC, VPL>, kThreads, smem));
+  int grid = std::max(1, std::min(P.total_tiles, sms * std::max(occ, 1)));
+  pack_fused_kernel<SRC, VPL><<<grid, kThreads, smem, s>>>(P);
+  KVF_CHECK_CUDA(cudaGetLastError());
+  return KVF_OK;
+}
+
+template <int SRC>
+kvf_status launch_fused_vpl(int vpl, const FusedParams& P, size_t smem, cudaStream_t s) {
+  switch (vpl) {
+    case 1: return launch_fused_t<SRC, 1>(P, smem, s);
+    case 2: return launch_fused_t<SRC, 2>(P, smem, s);
+    case 4: return launch_fused_t<SRC, 4>(P, smem, s);
+    case 8: return launch_fused_t<SRC, 8>(P, smem, s);
+    default: return launch_fused_t<SRC, 16>(P, smem, s);
+  }
+}
+
+kvf_status launch_fused_l2(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+                           cudaStream_t s) {
+  FusedParams* P = new FusedParams();
+  P->n_units = (int32_t)units.size();
+  P->n_sub = (int32_t)(3 * units.size());
+  int max_G = 1;
+  for (size_t k = 0; k < units.size(); ++k) {
+    P->u[k] = make_pack_unit_dev(units[k]);
+    max_G = std::max(max_G, P->u[k].G);
+  }
+  P->queue = P->u[0].done + 3;
+  int32_t acc = 0;
+  const int n_seg = P->n_sub + kLag;
+  for (int sidx = 0; sidx < n_seg; ++sidx) {
+    P->seg_begin[sidx] = acc;
+    int na = 0;
+    if (sidx < P->n_sub) {
+      const PackUnitDev& U = P->u[sidx / 3];
+      na = U.src.layer[sidx % 3] ? (U.g.T + kATok - 1) / kATok : 0;
+      P->n_a[sidx] = (uint16_t)na;
+    }
+    int nq = 0;
+    const int sq = sidx - kLag;
+    if (sq >= 0) nq = (P->u[sq / 3].n_items + kQItems - 1) / kQItems;
+    acc += na + nq;
+  }
+  P->seg_begin[n_seg] = acc;
+  P->total_tiles = acc;
+  size_t smem = (size_t)max_G * sizeof(uint32_t);
+  kvf_status st;
+  switch (dtype) {
+    case KVF_BF16: st = launch_fused_vpl<KVF_BF16>(vpl, *P, smem, s); break;
+    case KVF_F16: st = launch_fused_vpl<KVF_F16>(vpl, *P, smem, s); break;
+    default: st = launch_fused_vpl<KVF_F32>(vpl, *P, smem, s); break;
+  }
+  delete P;
+  return st;
+}
+
+// Both phases for fast-variant quantising units: zero the scratch, then the
+// cooperative TMA kernel, else the L2-reuse fused kernel.
+kvf_status launch_fused_group(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+                              cudaStream_t s) {
+  constexpr size_t kChunk = 64;  // units per fused launch
+  for (size_t at = 0; at < units.size(); at += kChunk) {
+    size_t n = std::min(kChunk, units.size() - at);
+    std::vector<kvf_pack_unit> part(units.begin() + at, units.begin() + at + n);
+    kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero scratch + counters
+    if (st != KVF_OK) return st;
+    bool launched = false;
+    st = launch_pack_coop(part, dtype, s, &launched);
+    if (st != KVF_OK) return st;
+    if (!launched) {
+      st = launch_fused_l2(part, vpl, dtype, s);
+      if (st != KVF_OK) return st;
     }
   }
   return KVF_OK;
 }
 
-kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases,
-               cudaStream_t s) {
-  if (n_units < 0 || (n_units > 0 && units == nullptr))
-    KVF_FAIL(KVF_EINVAL, "bad unit array");
+kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, cudaStream_t s) {
+  if (n_units < 0 || (n_units > 0 && units == nullptr)) KVF_FAIL(KVF_EINVAL, "bad unit array");
   std::vector<kvf_pack_unit> groups[17][4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
@@ -441,15 +649,20 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases,
   for (int v = 0; v <= 16; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        kvf_status st = launch_group(groups[v][dt], v, dt, phases, s);
+        // Default: the two-pass kernels (fastest measured); the
+        // single-read fused schedules are opt-in: KVF_PACK_MODE=fused.
+        const char* mode = getenv("KVF_PACK_MODE");
+        const bool fused = v != 0 && dt != KVF_I8 && phases == (1 | 2 | 4 | 8) && mode &&
+                           strcmp(mode, "fused") == 0;
+        kvf_status st = fused ? launch_fused_group(groups[v][dt], v, dt, s)
+                              : launch_phases(groups[v][dt], v, dt, phases, s);
         if (st != KVF_OK) return st;
       }
   return KVF_OK;
 }
 
-kvf_pack_unit single(const kvf_paged* src, const kvf_plan* plan,
-                     const uint32_t* absmax, float* scales,
-                     const kvf_surface* frames) {
+kvf_pack_unit single(const kvf_paged* src, const kvf_plan* plan, const uint32_t* absmax,
+                     float* scales, const kvf_surface* frames) {
   kvf_pack_unit u;
   u.src = *src;
   u.plan = *plan;
@@ -472,8 +685,7 @@ kvf_pack_unit single(const kvf_paged* src, const kvf_plan* plan,
 
 using namespace kvf;
 
-extern "C" kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
-                                     void* stream) {
+extern "C" kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units, void* stream) {
   return run(units, n_units, 1 | 2 | 4 | 8, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -481,8 +693,8 @@ extern "C" kvf_status kvf_pack_absmax(const kvf_paged* src, const kvf_plan* plan
                                       uint32_t* absmax, void* stream) {
   if (!src || !plan || !absmax) KVF_FAIL(KVF_EINVAL, "null argument");
   if (src->dtype == KVF_I8) KVF_FAIL(KVF_EINVAL, "int8 codes have no absmax phase");
-  float dummy_scales_never_written;
-  kvf_pack_unit u = single(src, plan, absmax, &dummy_scales_never_written, nullptr);
+  float unused_scales;
+  kvf_pack_unit u = single(src, plan, absmax, &unused_scales, nullptr);
   return run(&u, 1, 2, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -492,4 +704,9 @@ extern "C" kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan
   if (!src || !plan || !frames) KVF_FAIL(KVF_EINVAL, "null argument");
   kvf_pack_unit u = single(src, plan, absmax, scales, frames);
   return run(&u, 1, 4 | 8, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t kvf_pack_scratch_words(const kvf_plan* plan) {
+  if (!plan || check_plan(*plan) != KVF_OK) return -1;
+  return pack_scratch_words(*plan);
 }

@@ -24,16 +24,17 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kIPW = 2;  // items per warp
+constexpr int kIPW = 4;  // items per warp (loads in flight per lane: kIPW * VPL)
 
 struct RestoreUnitDev {
   kvf_surface fr;
   Geom g;
   const float* scales;
   kvf_paged dst;
+  FastDiv div_bs;
   int32_t first_frame;
-  int32_t n_items;  // n_frames * tiles_per_frame * 3
-  int32_t G;        // groups per layer
+  int32_t n_plane_items;  // n_frames * tiles_per_frame (per plane)
+  int32_t G;              // groups per layer
 };
 
 struct RestoreParams {
@@ -41,70 +42,52 @@ struct RestoreParams {
   RestoreUnitDev u[KVF_MAX_UNITS];
 };
 
-struct ItemPos {
-  int p, f, slot, i;
-};
-
-__device__ __forceinline__ ItemPos decode_item(const RestoreUnitDev& U,
-                                               int64_t j) {
-  ItemPos r;
-  int q = (int)(j / 3);
-  r.p = (int)(j - (int64_t)q * 3);
-  int fl = q / U.g.tpf;
-  r.slot = q - fl * U.g.tpf;
-  r.f = U.first_frame + fl;
-  r.i = token_of(U.g, r.f, r.slot);
-  return r;
-}
-
-__device__ __forceinline__ const uint8_t* tile_origin(const RestoreUnitDev& U,
-                                                      const ItemPos& x) {
-  int tr = x.slot / U.g.grid_cols;
-  int tc = x.slot - tr * U.g.grid_cols;
-  return U.fr.base + (int64_t)x.f * U.fr.frame_stride +
-         (int64_t)x.p * U.fr.plane_stride +
-         (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w;
-}
-
+// grid = (item tiles, unit, plane): the plane (layer of the triplet) is uniform
+// per CTA, so each lane loads its VPL group scales once and the per-item index
+// math is a handful of multiply-high divisions by host-precomputed constants.
 template <int OUT, int VPL>
 __global__ void __launch_bounds__(kThreads)
     restore_fast_kernel(const __grid_constant__ RestoreParams P) {
   const RestoreUnitDev& U = P.u[blockIdx.y];
+  const int p = blockIdx.z;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t item0 = ((int64_t)blockIdx.x * kWarps + warp) * kIPW;
-  if (item0 >= U.n_items) return;
+  const int item0 = (blockIdx.x * kWarps + warp) * kIPW;
+  char* layer = reinterpret_cast<char*>(U.dst.layer[p]);
+  if (item0 >= U.n_plane_items || layer == nullptr) return;
 
   constexpr int ES = OUT == KVF_F32 ? 4 : (OUT == KVF_I8 ? 1 : 2);
   int32_t in_off[VPL];
   int32_t out_off[VPL];
-  int32_t gidx[VPL];
+  float s[VPL];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     int c = (lane + 32 * k) * 8;
     in_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
-    out_off[k] = (int32_t)slot_channel_offset(U.g, c, U.dst.head_stride);
-    gidx[k] = c / U.g.group_size;
+    out_off[k] = (int32_t)slot_channel_offset(U.g, c, U.dst.head_stride) * ES;
+    if constexpr (OUT != KVF_I8) s[k] = __ldg(U.scales + p * U.G + (c >> U.g.lg_gs));
   }
+  const uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
 
   uint2 v[kIPW][VPL];
   char* outp[kIPW];
-  int plane[kIPW];
 #pragma unroll
   for (int it = 0; it < kIPW; ++it) {
     outp[it] = nullptr;
-    plane[it] = 0;
-    int64_t j = item0 + it;
-    if (j < U.n_items) {
-      ItemPos x = decode_item(U, j);
-      void* layer = U.dst.layer[x.p];
-      if (x.i < U.g.T && layer != nullptr) {
-        const uint8_t* src = tile_origin(U, x);
+    const int q = item0 + it;  // (frame, slot) item of this plane
+    if (q < U.n_plane_items) {
+      const int fl = fdiv(U.g.div_tpf, q);
+      const int slot = q - fl * U.g.tpf;
+      const int f = U.first_frame + fl;
+      const int i = token_of(U.g, f, slot);
+      if (i < U.g.T) {
+        const int tr = fdiv(U.g.div_cols, slot);
+        const int tc = slot - tr * U.g.grid_cols;
+        const uint8_t* src = plane_base + (int64_t)f * U.fr.frame_stride +
+                             (int64_t)tr * U.g.tile_h * U.fr.row_pitch + tc * U.g.tile_w;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) v[it][k] = ld_nc_v2(src + in_off[k]);
-        outp[it] = reinterpret_cast<char*>(layer) +
-                   paged_slot_offset(U.dst, x.i) * ES;
-        plane[it] = x.p;
+        outp[it] = layer + paged_slot_offset_fd(U.dst, U.div_bs, i) * ES;
       }
     }
   }
@@ -114,16 +97,15 @@ __global__ void __launch_bounds__(kThreads)
     if (outp[it] == nullptr) continue;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-      char* dst = outp[it] + (int64_t)out_off[k] * ES;
+      char* dst = outp[it] + out_off[k];
       if constexpr (OUT == KVF_I8) {
         // int8 code = u8 sample - 128 = sample ^ 0x80 (fk/fetchsim.py:351).
         st_v2(dst, make_uint2(v[it][k].x ^ 0x80808080u, v[it][k].y ^ 0x80808080u));
       } else {
-        const float s = __ldg(U.scales + plane[it] * U.G + gidx[k]);
         float q[8];
         bytes8_to_float(v[it][k].x, v[it][k].y, q);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) q[e] *= s;
+        for (int e = 0; e < 8; ++e) q[e] *= s[k];
         if constexpr (OUT == KVF_F32) {
           st_v4(dst, make_uint4(__float_as_uint(q[0]), __float_as_uint(q[1]),
                                 __float_as_uint(q[2]), __float_as_uint(q[3])));
@@ -145,20 +127,28 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     restore_generic_kernel(const __grid_constant__ RestoreParams P) {
   const RestoreUnitDev& U = P.u[blockIdx.y];
+  const int p = blockIdx.z;
   int64_t x = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-  int64_t j = x >> U.g.lg_C;
-  if (j >= U.n_items) return;
+  int64_t q_item = x >> U.g.lg_C;
+  void* layer = U.dst.layer[p];
+  if (q_item >= U.n_plane_items || layer == nullptr) return;
   int c = (int)(x & (U.g.C - 1));
-  ItemPos pos = decode_item(U, j);
-  void* layer = U.dst.layer[pos.p];
-  if (pos.i >= U.g.T || layer == nullptr) return;
-  const uint8_t* src = tile_origin(U, pos) + tile_offset(U.g, c, U.fr.row_pitch);
+  int fl = (int)q_item / U.g.tpf;
+  int slot = (int)q_item - fl * U.g.tpf;
+  int f = U.first_frame + fl;
+  int i = token_of(U.g, f, slot);
+  if (i >= U.g.T) return;
+  int tr = slot / U.g.grid_cols;
+  int tc = slot - tr * U.g.grid_cols;
+  const uint8_t* src = U.fr.base + (int64_t)f * U.fr.frame_stride +
+                       (int64_t)p * U.fr.plane_stride +
+                       (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w +
+                       tile_offset(U.g, c, U.fr.row_pitch);
   int q = (int)*src - 128;
   float val = 0.0f;
   if (U.dst.dtype != KVF_I8)
-    val = (float)q * __ldg(U.scales + pos.p * U.G + c / U.g.group_size);
-  int64_t o = paged_slot_offset(U.dst, pos.i) +
-              slot_channel_offset(U.g, c, U.dst.head_stride);
+    val = (float)q * __ldg(U.scales + p * U.G + c / U.g.group_size);
+  int64_t o = paged_slot_offset(U.dst, i) + slot_channel_offset(U.g, c, U.dst.head_stride);
   store_from_float(layer, o, U.dst.dtype, val, q);
 }
 
@@ -206,6 +196,8 @@ kvf_status check_unit(const kvf_restore_unit& u) {
     KVF_FAIL(KVF_EINVAL, "dequantising restore needs scales");
   if (u.dst.block_size < 1) KVF_FAIL(KVF_EINVAL, "block_size must be >= 1");
   if (u.dst.token_base < 0) KVF_FAIL(KVF_EINVAL, "negative token_base");
+  if ((int64_t)u.dst.token_base + u.plan.T >= (int64_t(1) << 31))
+    KVF_FAIL(KVF_EUNSUPPORTED, "token index beyond 2^31");
   return KVF_OK;
 }
 
@@ -215,8 +207,9 @@ RestoreUnitDev to_dev(const kvf_restore_unit& u) {
   d.g = make_geom(u.plan);
   d.scales = u.scales;
   d.dst = u.dst;
+  d.div_bs = make_fastdiv(u.dst.block_size);
   d.first_frame = u.first_frame;
-  d.n_items = u.n_frames * u.plan.tiles_per_frame * 3;
+  d.n_plane_items = u.n_frames * u.plan.tiles_per_frame;
   d.G = (u.plan.H * u.plan.D) / u.plan.group_size;
   return d;
 }
@@ -242,14 +235,14 @@ kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
     int64_t max_work = 0;
     for (size_t k = 0; k < n; ++k) {
       P.u[k] = to_dev(units[at + k]);
-      int64_t w = vpl ? P.u[k].n_items : (int64_t)P.u[k].n_items * P.u[k].g.C;
+      int64_t w = vpl ? P.u[k].n_plane_items : (int64_t)P.u[k].n_plane_items * P.u[k].g.C;
       max_work = std::max(max_work, w);
     }
     if (max_work == 0) continue;
     int64_t per_cta = vpl ? (int64_t)kWarps * kIPW : kThreads;
     int64_t gx = (max_work + per_cta - 1) / per_cta;
     if (gx > 0x7FFFFFFF) KVF_FAIL(KVF_EUNSUPPORTED, "restore grid too large");
-    dim3 grid((unsigned)gx, (unsigned)n);
+    dim3 grid((unsigned)gx, (unsigned)n, 3);
     if (vpl == 0) {
       restore_generic_kernel<<<grid, kThreads, 0, s>>>(P);
     } else {

@@ -103,7 +103,8 @@ def test_fused_pack_matches_oracle(lay, res):
         for T0, Tc in chunks:
             plan = L.plan_inter_frame(Tc, res, L.LayoutConfig(*lay), 4)
             fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
-            am = torch.empty((3, H * D // gs), dtype=torch.int32, device="cuda")
+            am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)), dtype=torch.int32,
+                             device="cuda")
             sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
             u, plan = _pack_unit(kv, lay, res, T0, Tc, 4, gs, fr, am, sc, trip)
             units.append(u)
@@ -141,11 +142,9 @@ def test_restore_paged_matches_oracle(lay, dtype):
     T, res = 333, "R480"
     x, v, s, frames = _oracle_chunk(T, lay, res, seed=4, gs=gs)
     plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
-    mem = KV.PagedMemory(16, dtype=dtype)
+    mem = KV.PagedMemory(16, dtype=dtype, H=H, D=D, num_blocks=64, num_layers=6)
     mem.begin_fetch()
     # scatter the logical pages over a shuffled physical pool
-    mem._ensure_layers(6)
-    mem._ensure_blocks(64)
     rng = np.random.default_rng(0)
     mem._free = list(rng.permutation(mem._free))
     n = restore_frames(torch.from_numpy(frames).cuda(), plan, mem, layer_base=3,
@@ -273,7 +272,8 @@ def test_c2_unit_round_trip_property():
     lay = (8, 128, 1, 8, 1, 128)
     plan = L.plan_inter_frame(T, "R1080", L.LayoutConfig(*lay), 4)
     fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
-    am = torch.empty((3, 8), dtype=torch.int32, device="cuda")
+    am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)), dtype=torch.int32,
+                     device="cuda")
     sc = torch.empty((3, 8), dtype=torch.float32, device="cuda")
     u, _ = _pack_unit(kv.data, lay, "R1080", 0, T, 4, gs, fr, am, sc)
     _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
