@@ -208,6 +208,108 @@ kvf_status kvf_dequantize(const int8_t* values, const float* scales, int64_t T,
                           int32_t L, int32_t C, int32_t group_size, void* out,
                           int32_t out_dtype, void* stream);
 
+/* ---- KVFC bitstream decode (fk/codec.py:155-211) -------------------------- */
+
+/* Stream geometry from the 12-byte header (u32 n_frames, height, width). */
+typedef struct kvf_kvfc_info {
+  int32_t n_frames;
+  int32_t height;
+  int32_t width;
+  int32_t bitmap_len;      /* bytes of one packed mode bitmap: ceil(bh*bw/8) */
+} kvf_kvfc_info;
+
+/* Host-side walk of a KVFC stream (fk/codec.py:16-20 layout) exactly as
+ * decode_frames walks it (fk/codec.py:164-208), without entropy decoding.
+ * For frame f, plane p (k = 3f + p): payload_off[k], payload_len[k] (the u32
+ * length prefix), bitmap_off[k] (-1 for intra frames); frame_type[f].
+ * Arrays hold cap_frames frames (3*cap_frames entries); with cap_frames <
+ * n_frames only `info` is filled and KVF_EINVAL is returned.  Returns
+ * KVF_EDECODE and *bad_frame on every condition where the reference raises
+ * DecodeError (short header, truncated type/bitmap/length/payload, bad frame
+ * type, inter frame without reference, trailing bytes). */
+kvf_status kvf_kvfc_scan(const uint8_t* data, int64_t size, kvf_kvfc_info* info,
+                         int64_t* payload_off, int32_t* payload_len,
+                         int64_t* bitmap_off, uint8_t* frame_type,
+                         int32_t cap_frames, int32_t* bad_frame);
+
+/* One range-coded symbol stream (one plane of one frame). */
+typedef struct kvf_rc_stream {
+  const uint8_t* payload;  /* device */
+  int64_t len;             /* payload bytes (reads past the end yield 0) */
+  uint8_t* symbols;        /* device output */
+  int64_t n_symbols;       /* height * width */
+} kvf_rc_stream;
+
+/* Entropy-decode n_streams independent streams (fk/rangecoder.py:146-189:
+ * adaptive order-0 model reset per stream, carry-less 32-bit range coder),
+ * one GPU thread per stream.  `d_streams` is a DEVICE array. */
+kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_streams,
+                         void* stream);
+
+/* One plane of one frame for reconstruction (fk/codec.py:131-144). */
+typedef struct kvf_recon_plane {
+  const uint8_t* symbols;  /* device, height*width zigzag symbols */
+  const uint8_t* modes;    /* device packed mode bitmap (np.packbits order), NULL = intra */
+  uint8_t* out;            /* device plane origin */
+  int64_t out_pitch;       /* bytes between rows */
+} kvf_recon_plane;
+
+/* A dependency chain: planes[first .. first+count) of ONE plane index over
+ * consecutive frames, the first intra; entry k predicts from entry k-1. */
+typedef struct kvf_recon_chain {
+  int32_t first;
+  int32_t count;
+  int32_t height;
+  int32_t width;
+} kvf_recon_chain;
+
+/* Reconstruct every chain (one CTA per chain; frames inside a chain in order):
+ * sample = (pred + unzigzag(symbol)) mod 256 with pred = co-located previous
+ * frame sample (inter block), left neighbour, first column from above, 128 at
+ * the corner.  Both arrays are DEVICE arrays. */
+kvf_status kvf_kvfc_reconstruct(const kvf_recon_plane* d_planes,
+                                const kvf_recon_chain* d_chains, int32_t n_chains,
+                                void* stream);
+
+/* ---- KVFC bitstream encode (fk/codec.py:93-128) ------------------------- */
+
+/* One plane of one frame to predict: residuals, 16x16 modes, zigzag symbols. */
+typedef struct kvf_resid_plane {
+  const uint8_t* cur;      /* device plane origin */
+  const uint8_t* prev;     /* previous frame's plane, NULL for an intra frame */
+  int64_t pitch;           /* bytes between rows of cur (and prev) */
+  uint8_t* symbols;        /* device out: height*width zigzag symbols */
+  uint8_t* modes;          /* device out: bh*bw bytes, 1 = inter (inter frames only) */
+  int32_t height;
+  int32_t width;
+} kvf_resid_plane;
+
+/* Per 16x16 block: intra residual (left; first column from above; 128 at the
+ * corner) and, for inter frames, the co-located inter residual; mode = inter
+ * iff SAD_inter <= SAD_intra (fk/codec.py:77-90, 110-123); symbols =
+ * zigzag(residual mod 256).  `d_planes` is a DEVICE array. */
+kvf_status kvf_kvfc_residuals(const kvf_resid_plane* d_planes, int32_t n_planes,
+                              int32_t max_blocks, void* stream);
+
+/* Range-encode n streams (fk/rangecoder.py:106-143), one thread per stream:
+ * reads `symbols`/`n_symbols`, writes `payload` (capacity >= 2*n_symbols + 16)
+ * and the coded length to d_out_len[k].  `d_streams` is a DEVICE array. */
+kvf_status kvf_rc_encode(const kvf_rc_stream* d_streams, int32_t n_streams,
+                         int64_t* d_out_len, void* stream);
+
+/* Scatter pieces into a stream buffer: dst[dst_off .. +len) = src[0 .. len),
+ * or, with pack_bits, dst[dst_off + b/8] bit (7 - b%8) = src[b] for b < len
+ * (np.packbits order).  `d_pieces` is a DEVICE array. */
+typedef struct kvf_piece {
+  const uint8_t* src;
+  int64_t dst_off;
+  int64_t len;
+  int32_t pack_bits;
+  int32_t reserved_;
+} kvf_piece;
+kvf_status kvf_gather(const kvf_piece* d_pieces, int32_t n_pieces, uint8_t* dst,
+                      void* stream);
+
 /* ---- synthetic inputs ---------------------------------------------------- */
 
 /* In-place AR(1) scan along the middle axis of an fp32 [outer, len, inner]

@@ -73,12 +73,61 @@ class kvf_pack_unit(C.Structure):
     ]
 
 
-class kvf_kvfc_index(C.Structure):
+class kvf_kvfc_info(C.Structure):
     _fields_ = [
         ("n_frames", C.c_int32),
         ("height", C.c_int32),
         ("width", C.c_int32),
         ("bitmap_len", C.c_int32),
+    ]
+
+
+class kvf_rc_stream(C.Structure):
+    _fields_ = [
+        ("payload", C.c_void_p),
+        ("len", C.c_int64),
+        ("symbols", C.c_void_p),
+        ("n_symbols", C.c_int64),
+    ]
+
+
+class kvf_recon_plane(C.Structure):
+    _fields_ = [
+        ("symbols", C.c_void_p),
+        ("modes", C.c_void_p),
+        ("out", C.c_void_p),
+        ("out_pitch", C.c_int64),
+    ]
+
+
+class kvf_resid_plane(C.Structure):
+    _fields_ = [
+        ("cur", C.c_void_p),
+        ("prev", C.c_void_p),
+        ("pitch", C.c_int64),
+        ("symbols", C.c_void_p),
+        ("modes", C.c_void_p),
+        ("height", C.c_int32),
+        ("width", C.c_int32),
+    ]
+
+
+class kvf_piece(C.Structure):
+    _fields_ = [
+        ("src", C.c_void_p),
+        ("dst_off", C.c_int64),
+        ("len", C.c_int64),
+        ("pack_bits", C.c_int32),
+        ("reserved_", C.c_int32),
+    ]
+
+
+class kvf_recon_chain(C.Structure):
+    _fields_ = [
+        ("first", C.c_int32),
+        ("count", C.c_int32),
+        ("height", C.c_int32),
+        ("width", C.c_int32),
     ]
 
 
@@ -102,6 +151,13 @@ _SIGNATURES = {
     "kvf_dequantize": (C.c_int, [_VP, _VP, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                  _VP, C.c_int32, _VP]),
     "kvf_ar1_scan": (C.c_int, [_VP, C.c_int64, C.c_int64, C.c_int64, C.c_float, _VP]),
+    "kvf_kvfc_scan": (C.c_int, [_VP, C.c_int64, C.POINTER(kvf_kvfc_info), _VP, _VP, _VP, _VP,
+                                C.c_int32, C.POINTER(C.c_int32)]),
+    "kvf_rc_decode": (C.c_int, [_VP, C.c_int32, _VP]),
+    "kvf_kvfc_reconstruct": (C.c_int, [_VP, _VP, C.c_int32, _VP]),
+    "kvf_kvfc_residuals": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP]),
+    "kvf_rc_encode": (C.c_int, [_VP, C.c_int32, _VP, _VP]),
+    "kvf_gather": (C.c_int, [_VP, C.c_int32, _VP, _VP]),
 }
 
 _lib = None

@@ -17,7 +17,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libkvf.so")
 
 SOURCES = ["kvf_api.cu", "kvf_restore.cu", "kvf_pack.cu", "kvf_pack_coop.cu", "kvf_kvfc.cu",
-           "kvf_kvfc_host.cpp"]
+           "kvf_kvfc_enc.cu", "kvf_kvfc_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]

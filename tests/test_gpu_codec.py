@@ -1,0 +1,114 @@
+"""GPU KVFC decode (range decoder + predictor kernels) is bit-exact against the
+reference decoder: golden streams, random sequences/GOPs, all 48 tilings of a
+32x128 cache at R240 (tests/test_acceptance.py:112-145 of the reference), and
+many streams decoded in one batch."""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_09725_b200 import codec  # noqa: E402
+
+
+def test_golden_streams_decode(golden):
+    for c in golden["codec"]:
+        fr = cases.codec_frames(c)
+        bs = ref.encode_frames(fr, c["gop"])
+        assert ref.digest(bs) == c["stream"]
+        got = []
+        n = codec.decode_frames(bs, codec.CodecConfig(gop=c["gop"]),
+                                lambda f, x: got.append(x.cpu().numpy()))
+        assert n == fr.shape[0]
+        assert np.array_equal(np.stack(got), fr), c
+
+
+def test_random_sequences_batched():
+    rng = np.random.default_rng(5)
+    frames, streams = [], []
+    for _ in range(300):
+        n = int(rng.integers(1, 6))
+        h = int(rng.integers(4, 40))
+        w = int(rng.integers(4, 70))
+        kind = int(rng.integers(0, 3))
+        if kind == 0:
+            fr = rng.integers(0, 256, size=(n, 3, h, w)).astype(np.uint8)
+        elif kind == 1:
+            base = rng.integers(0, 256, size=(1, 3, h, w))
+            fr = np.clip(base + rng.integers(-6, 7, size=(n, 3, h, w)), 0, 255).astype(np.uint8)
+        else:
+            fr = np.full((n, 3, h, w), int(rng.integers(0, 256)), np.uint8)
+        gop = int(rng.integers(1, 5))
+        frames.append(fr)
+        streams.append(ref.encode_frames(fr, gop))
+    out, _ = codec.decode_batch(streams)
+    for fr, o in zip(frames, out):
+        assert np.array_equal(o.cpu().numpy(), fr)
+
+
+def test_all_tilings_32x128_r240():
+    x = ref.gen_synthetic_kv(8, 3, 32, 128, 0.9, 0, 0.3)
+    v, _ = ref.quantize(x, 128)
+    t = v.reshape(8, 3, 32 * 128)
+    streams, frames = [], []
+    for a_h in (1, 2, 4, 8, 16, 32):
+        for a_d in (1, 2, 4, 8, 16, 32, 64, 128):
+            plan = ref.Plan(8, "R240", 32, 128, a_h, 32 // a_h, a_d, 128 // a_d, F=4)
+            fr = ref.assemble_frames(t, plan)
+            frames.append(fr)
+            streams.append(ref.encode_frames(fr, 4))
+    assert len(streams) == 48
+    out, _ = codec.decode_batch(streams)
+    for fr, o in zip(frames, out):
+        assert np.array_equal(o.cpu().numpy(), fr)
+
+
+def test_large_r1080_chunk_and_pitched_output():
+    fr = cases.codec_frames(dict(kind="kv", layout=[8, 128, 1, 8, 1, 128], T=2000, res="R1080",
+                                 gop=4, seed=3, n=0, h=0, w=0))
+    bs = ref.encode_frames(fr, 4)
+    n, _, h, w = fr.shape
+    big = torch.zeros((n, 3, h, w + 64), dtype=torch.uint8, device="cuda")
+    view = big[:, :, :, :w]
+    out, _ = codec.decode_batch([bs], out=[view])
+    assert np.array_equal(view.cpu().numpy(), fr)
+    assert torch.all(big[:, :, :, w:] == 0)
+
+
+def test_decode_errors():
+    fr = cases.codec_frames(dict(kind="jitter", n=3, h=8, w=8, gop=2, seed=1))
+    bs = ref.encode_frames(fr, 2)
+    for bad in (bs[:5], bs[:-3], bs + b"\0"):
+        with pytest.raises(codec.DecodeError):
+            codec.decode_frames(bad, codec.CodecConfig(gop=2), lambda f, x: None)
+
+
+def test_encode_bit_exact_vs_reference(golden):
+    for c in golden["codec"]:
+        fr = cases.codec_frames(c)
+        bs = codec.encode_frames(torch.from_numpy(fr).cuda(), codec.CodecConfig(gop=c["gop"]))
+        assert ref.digest(bs.data) == c["stream"], c
+        assert bs.frame_count == fr.shape[0]
+
+
+def test_encode_batch_random_round_trip():
+    rng = np.random.default_rng(7)
+    frames, gops = [], []
+    for _ in range(120):
+        n = int(rng.integers(1, 6))
+        h = int(rng.integers(4, 40))
+        w = int(rng.integers(4, 70))
+        base = rng.integers(0, 256, size=(1, 3, h, w))
+        fr = np.clip(base + rng.integers(-9, 10, size=(n, 3, h, w)), 0, 255).astype(np.uint8)
+        frames.append(fr)
+        gops.append(int(rng.integers(1, 5)))
+    out = codec.encode_batch([torch.from_numpy(f).cuda() for f in frames], gops)
+    for fr, g, bs in zip(frames, gops, out):
+        assert bs.data == ref.encode_frames(fr, g)
+    dec, _ = codec.decode_batch(out)
+    for fr, d in zip(frames, dec):
+        assert np.array_equal(d.cpu().numpy(), fr)

@@ -1,0 +1,84 @@
+"""Host-side KVFC stream walk (kvf_kvfc_scan, C++ in libkvf): offsets and the
+DecodeError conditions match the reference decoder (via the pinned oracle)."""
+
+import struct
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import ref
+from paper_2602_09725_b200.codec import DecodeError, StreamIndex
+
+
+def _walk(data):
+    """Independent Python walk of fk/codec.py:16-20 for offsets."""
+    n, h, w = struct.unpack_from("<III", data, 0)
+    blen = ((-(-h // 16)) * (-(-w // 16)) + 7) // 8
+    pos, out = 12, []
+    for f in range(n):
+        t = data[pos]
+        pos += 1
+        for p in range(3):
+            boff = -1
+            if t == 1:
+                boff = pos
+                pos += blen
+            (plen,) = struct.unpack_from("<I", data, pos)
+            pos += 4
+            out.append((pos, plen, boff))
+            pos += plen
+    return n, h, w, out
+
+
+@pytest.mark.parametrize("k", range(len(cases.CODEC_CASES)))
+def test_scan_offsets(k):
+    c = cases.CODEC_CASES[k]
+    bs = ref.encode_frames(cases.codec_frames(c), c["gop"])
+    ix = StreamIndex(bs)
+    n, h, w, want = _walk(bs)
+    assert (ix.n, ix.h, ix.w) == (n, h, w)
+    for j, (off, plen, boff) in enumerate(want):
+        assert ix.payload_off[j] == off and ix.payload_len[j] == plen and ix.bitmap_off[j] == boff
+    for f in range(n):
+        assert ix.frame_type[f] == (0 if f % c["gop"] == 0 else 1)
+
+
+def _oracle_error(data):
+    try:
+        ref.decode_frames(data)
+    except ref.OracleDecodeError as e:
+        return e.frame_index
+    return None
+
+
+def test_scan_errors_match_reference_decoder():
+    rng = np.random.default_rng(3)
+    fr = cases.codec_frames(dict(kind="jitter", n=5, h=20, w=37, gop=3, seed=9))
+    bs = ref.encode_frames(fr, 3)
+    variants = [bs[:5], bs[:12], bs[:13], bs[:-1], bs + b"\x00", bs[:40]]
+    bad_type = bytearray(bs)
+    bad_type[12] = 7
+    variants.append(bytes(bad_type))
+    inter_first = bytearray(bs)
+    inter_first[12] = 1
+    variants.append(bytes(inter_first))
+    for cut in rng.integers(12, len(bs), size=40):
+        variants.append(bs[:int(cut)])
+    for v in variants:
+        want = _oracle_error(v)
+        if want is None:
+            StreamIndex(v)
+            continue
+        with pytest.raises(DecodeError) as ei:
+            StreamIndex(v)
+        assert ei.value.frame_index == want, (len(v), want, ei.value.frame_index)
+
+
+def test_empty_stream():
+    data = struct.pack("<III", 0, 4, 4)
+    ix = StreamIndex(data)
+    assert ix.n == 0
+    with pytest.raises(DecodeError) as ei:
+        StreamIndex(data + b"\x01")
+    assert ei.value.frame_index == -1  # the reference reports frame n-1
