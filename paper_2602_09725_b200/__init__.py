@@ -1,0 +1,18 @@
+"""B200-native (sm_100a) KV-frame hot path of KVFetcher (arXiv 2602.09725).
+
+Drop-in for the reference ``framekv`` package's data path, with the same module
+names and entry points:
+
+  kvmodel   - KVCache, QuantizedKV, quantize/dequantize, PagedMemory (GPU)
+  layout    - LayoutConfig, FramePlan, assemble_frames/disassemble_frames (GPU)
+  codec     - KVFC frame codec: GPU range decoder/encoder + predictor
+  container - KVFC chunk container: pack_chunk / unpack_chunk
+  restore   - restore_stream / restore_chunk_wise / restore_frames (GPU, fused dequant)
+  netstore  - chunk server + wire protocol (host transport, reference-compatible)
+  fetch     - live_fetch_pipeline: network receive || GPU decode + restore
+
+Every data-path call goes through libkvf.so (include/kvf.h); there is no CPU
+fallback — importing works without a GPU, calling a kernel does not.
+"""
+
+__version__ = "0.1.0"

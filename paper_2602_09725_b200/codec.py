@@ -94,43 +94,68 @@ def _to_device_struct_array(arr, device) -> torch.Tensor:
     return torch.from_numpy(raw.copy()).to(device)
 
 
-def decode_batch(streams, out=None, stream=None):
+def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     """Decode many KVFC streams on the GPU in one pair of launches.
 
     ``streams``: list of bytes / Bitstream.  ``out``: optional list of
-    [n, 3, h, w] uint8 CUDA tensors (any row pitch) to decode into.  Returns
-    (frames list, device bytes held).  Raises DecodeError like the reference.
+    [n, 3, h, w] uint8 CUDA tensors (any row pitch) to decode into.
+    ``ranges``: optional per-stream (first, stop) frame range; ``first`` must
+    be an intra frame (a chain start), and the output holds stop-first frames.
+    Returns (frames list, device bytes held).  Raises DecodeError like the
+    reference.
     """
     dev = _dev.device()
     datas = [_as_bytes(s) for s in streams]
-    idxs = [StreamIndex(d) for d in datas]
-    starts = np.cumsum([0] + [len(d) for d in datas])
+    idxs = indices if indices is not None else [StreamIndex(d) for d in datas]
+    if ranges is None:
+        ranges = [(0, ix.n) for ix in idxs]
+    for ix, (f0, f1) in zip(idxs, ranges):
+        if not 0 <= f0 <= f1 <= ix.n:
+            raise ValueError("frame range outside the stream")
+        if f0 < f1 and ix.frame_type[f0] != 0:
+            raise ValueError("a partial decode must start at an intra frame")
+    # Only the byte span of the decoded frames travels to the device.
+    spans = []
+    for ix, (f0, f1) in zip(idxs, ranges):
+        if f1 <= f0:
+            spans.append((0, 0))
+            continue
+        ks = slice(3 * f0, 3 * f1)
+        heads = np.where(ix.bitmap_off[ks] >= 0, ix.bitmap_off[ks], ix.payload_off[ks])
+        spans.append((int(heads.min()),
+                      int((ix.payload_off[ks] + ix.payload_len[ks]).max())))
+    sizes = [hi - lo for lo, hi in spans]
+    starts = np.cumsum([0] + sizes)
     host = torch.empty(int(starts[-1]) or 1, dtype=torch.uint8, pin_memory=True)
     hv = host.numpy()
-    for d, s0 in zip(datas, starts[:-1]):
-        hv[s0:s0 + len(d)] = np.frombuffer(d, np.uint8)
+    for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
+        hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
+    # shift so that stream offsets index the copied span
+    starts = starts - np.array([lo for lo, _ in spans] + [0])
     s = stream if stream is not None else torch.cuda.current_stream()
     with torch.cuda.stream(s):
         blob = host.to(dev, non_blocking=True)
         frames = []
-        n_sym = sum(3 * ix.n * ix.h * ix.w for ix in idxs)
+        n_fr = [f1 - f0 for f0, f1 in ranges]
+        n_sym = sum(3 * nf * ix.h * ix.w for nf, ix in zip(n_fr, idxs))
         symbols = torch.empty(max(n_sym, 1), dtype=torch.uint8, device=dev)
-        rc = (_lib.kvf_rc_stream * max(1, sum(3 * ix.n for ix in idxs)))()
-        planes = (_lib.kvf_recon_plane * max(1, sum(3 * ix.n for ix in idxs)))()
+        rc = (_lib.kvf_rc_stream * max(1, 3 * sum(n_fr)))()
+        planes = (_lib.kvf_recon_plane * max(1, 3 * sum(n_fr)))()
         chains = []
         k_rc = 0
         sym_at = 0
         base = blob.data_ptr()
         sym_base = symbols.data_ptr()
-        for j, ix in enumerate(idxs):
-            fr = out[j] if out is not None else torch.empty((ix.n, 3, ix.h, ix.w),
+        for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
+            nf = f1 - f0
+            fr = out[j] if out is not None else torch.empty((nf, 3, ix.h, ix.w),
                                                            dtype=torch.uint8, device=dev)
-            if tuple(fr.shape) != (ix.n, 3, ix.h, ix.w):
+            if tuple(fr.shape) != (nf, 3, ix.h, ix.w):
                 raise ValueError("output frames have the wrong shape")
             frames.append(fr)
             hw = ix.h * ix.w
             plane_at = k_rc
-            for f in range(ix.n):
+            for f in range(f0, f1):
                 for p in range(3):
                     k = 3 * f + p
                     e = rc[k_rc]
@@ -141,21 +166,21 @@ def decode_batch(streams, out=None, stream=None):
                     q = planes[k_rc]
                     q.symbols = sym_base + sym_at
                     q.modes = (base + int(starts[j] + ix.bitmap_off[k])) if ix.bitmap_off[k] >= 0 else None
-                    q.out = fr[f, p].data_ptr()
+                    q.out = fr[f - f0, p].data_ptr()
                     q.out_pitch = fr.stride(2)
                     sym_at += hw
                     k_rc += 1
             if hw == 0:
                 continue
             # chains: runs of frames starting at each intra frame, per plane
-            f = 0
-            while f < ix.n:
+            f = f0
+            while f < f1:
                 g = f + 1
-                while g < ix.n and ix.frame_type[g] == 1:
+                while g < f1 and ix.frame_type[g] == 1:
                     g += 1
                 for p in range(3):
                     # entries of plane p for frames f..g-1 are strided by 3
-                    chains.append((plane_at, f, g, p, ix.h, ix.w))
+                    chains.append((plane_at, f - f0, g - f0, p, ix.h, ix.w))
                 f = g
         # re-pack planes so each chain's entries are contiguous
         flat = (_lib.kvf_recon_plane * max(1, k_rc))()

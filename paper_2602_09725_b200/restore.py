@@ -65,6 +65,54 @@ def restore_frames(frames: torch.Tensor, plan: FramePlan, mem: PagedMemory,
     return len(toks)
 
 
+def _chain_batches(ix, batch_frames):
+    """Frame ranges of at least batch_frames frames, each starting at an intra frame."""
+    starts = [f for f in range(ix.n) if ix.frame_type[f] == 0]
+    out, f0 = [], 0
+    for s in starts[1:] + [ix.n]:
+        if s - f0 >= batch_frames or s == ix.n:
+            out.append((f0, s))
+            f0 = s
+    return [r for r in out if r[1] > r[0]]
+
+
+def restore_stream(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_base=0,
+                   token_base=0, *, scales=None, batch_frames=None, real_layers=None):
+    """Frame-wise restore of one KVFC stream into paged memory (fk/fetchsim.py:335-358).
+
+    Decodes on the GPU and restores each decoded frame batch with one libkvf
+    launch.  ``batch_frames=None`` decodes the whole chunk at once (maximum
+    decoder parallelism); a small value (e.g. plan.F) bounds the live decode
+    buffers to that many frames, the reference's frame-wise memory profile.
+    Returns {"tokens_written", "peak_buffer_bytes"} like the reference.
+    """
+    from . import codec
+
+    data = codec._as_bytes(bs)
+    ix = codec.StreamIndex(data)
+    if (ix.n, ix.h, ix.w) != (plan.frame_count, plan.frame_h, plan.frame_w):
+        raise ValueError("stream geometry does not match the plan")
+    ranges = [(0, ix.n)] if batch_frames is None else _chain_batches(ix, int(batch_frames))
+    written, peak = 0, 0
+    for f0, f1 in ranges:
+        frames, held = codec.decode_batch([data], ranges=[(f0, f1)], indices=[ix])
+        peak = max(peak, held)
+        written += restore_frames(frames[0], plan, mem, layer_base, token_base, scales=scales,
+                                  first_frame=f0, n_frames=f1 - f0, real_layers=real_layers)
+    return {"tokens_written": written, "peak_buffer_bytes": peak}
+
+
+def restore_chunk_wise(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_base=0,
+                       token_base=0, *, scales=None, real_layers=None):
+    """Baseline: decode every frame, then restore (fk/fetchsim.py:361-385)."""
+    from . import codec
+
+    frames, held = codec.decode_batch([bs])
+    written = restore_frames(frames[0], plan, mem, layer_base, token_base, scales=scales,
+                             real_layers=real_layers)
+    return {"tokens_written": written, "peak_buffer_bytes": held}
+
+
 def restore_units(units, stream=None) -> None:
     """Batched restore of prepared kvf_restore_unit descriptors (one call, few launches)."""
     arr = (_lib.kvf_restore_unit * len(units))(*units)

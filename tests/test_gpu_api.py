@@ -1,0 +1,165 @@
+"""Drop-in API on the GPU, mirroring the reference's own tests for the path:
+container pack/unpack (tests/test_container.py:25-50), frame-wise restore
+(tests/test_fetchsim.py:255-282, tests/test_acceptance.py:224-243) and the
+loopback fetch (tests/test_acceptance.py:148-166)."""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_09725_b200 import container as C  # noqa: E402
+from paper_2602_09725_b200 import fetch as FE  # noqa: E402
+from paper_2602_09725_b200 import kvmodel as KV  # noqa: E402
+from paper_2602_09725_b200 import layout as L  # noqa: E402
+from paper_2602_09725_b200 import netstore as NS  # noqa: E402
+from paper_2602_09725_b200.restore import restore_chunk_wise, restore_stream  # noqa: E402
+
+
+def _q(kvc):
+    x = cases.quant_input(kvc)
+    src = torch.from_numpy(x)
+    if kvc.get("bf16"):
+        src = src.to(torch.bfloat16)
+    return KV.quantize(KV.KVCache(src.cuda()), kvc["group_size"]), x
+
+
+def test_container_bytes_match_reference(golden):
+    for c in golden["container"]:
+        q, _ = _q(c["kv"])
+        cont = C.pack_chunk(q, L.LayoutConfig(*c["layout"]), c["res"],
+                            cache_id=bytes.fromhex(c["cache_id"]), chunk_index=c["chunk_index"],
+                            token_start=c["token_start"], layer_triplet_index=c["triplet"],
+                            F=c["F"])
+        blob = cont.to_bytes()
+        assert ref.digest(blob) == c["bytes"]
+        back = C.ChunkContainer.from_bytes(blob)
+        for code in back.resolutions:
+            slab = C.unpack_chunk(back, code)
+            assert torch.equal(slab.values, q.values)
+            assert torch.equal(slab.scales, q.scales)
+            assert slab.group_size == q.group_size
+
+
+def test_pack_metadata_contents():
+    q, _ = _q(dict(kind="synthetic", T=17, L=3, H=4, D=8, s=0.9, seed=0, c=0.0, group_size=8))
+    cfg = L.identity_layout(4, 8)
+    c = C.pack_chunk(q, cfg, ["R240", "R1080"], token_start=170, layer_triplet_index=2)
+    assert (c.token_count, c.token_start, c.layer_triplet_index) == (17, 170, 2)
+    assert c.layout() == cfg and c.metadata["F"] == 4
+    assert set(c.metadata["plans"]) == {"R240", "R1080"}
+    assert c.metadata["frame_counts"]["R240"] == c.plan(0).frame_count
+    assert np.array_equal(c.scales(), q.scales.cpu().numpy())
+    with pytest.raises(ValueError):
+        C.pack_chunk(q, cfg, [])
+    with pytest.raises(ValueError):
+        C.pack_chunk(q, cfg, ["R240"], max_tokens=10)
+
+
+@pytest.mark.parametrize("dtype", [torch.int8, torch.bfloat16])
+def test_restore_stream_matches_chunk_wise_and_golden(golden, dtype):
+    for c in golden["restore"]:
+        q, x = _q(c["kv"])
+        cfg = L.LayoutConfig(*c["layout"])
+        cont = C.pack_chunk(q, cfg, [c["res"]], F=c["F"])
+        code = L.RESOLUTION_CODE[c["res"]]
+        bs, plan = cont.bitstream(code), cont.plan(code)
+        assert ref.digest(bs) == c["stream"]
+        mem_a = KV.PagedMemory(c["page"], dtype=dtype)
+        mem_a.begin_fetch()
+        out_a = restore_stream(bs, plan, cfg, mem_a, c["layer_base"], c["token_base"],
+                               scales=q.scales, batch_frames=plan.F)
+        mem_b = KV.PagedMemory(c["page"], dtype=dtype)
+        mem_b.begin_fetch()
+        out_b = restore_chunk_wise(bs, plan, cfg, mem_b, c["layer_base"], c["token_base"],
+                                   scales=q.scales)
+        T = c["kv"]["T"]
+        assert out_a["tokens_written"] == out_b["tokens_written"] == T
+        # The GPU decodes at least one GOP (inter frames chain on the previous
+        # frame); a single-GOP chunk therefore holds the same bytes both ways.
+        if plan.frame_count > plan.F:
+            assert out_a["peak_buffer_bytes"] < out_b["peak_buffer_bytes"]
+        else:
+            assert out_a["peak_buffer_bytes"] <= out_b["peak_buffer_bytes"]
+        deq = KV.dequantize(q, torch.bfloat16).data
+        blob = b""
+        for t in range(T):
+            for l in range(3):
+                a = mem_a.read(c["token_base"] + t, c["layer_base"] + l)
+                b = mem_b.read(c["token_base"] + t, c["layer_base"] + l)
+                assert torch.equal(a, b)
+                if dtype == torch.int8:
+                    blob += a.cpu().numpy().tobytes()
+                else:
+                    assert torch.equal(a, deq[t, l].reshape(-1))
+        if dtype == torch.int8:
+            assert ref.digest(blob) == c["slots"]
+            assert mem_a.allocated_bytes == c["allocated_bytes"]
+        with pytest.raises(KV.ConflictError):
+            restore_stream(bs, plan, cfg, mem_a, c["layer_base"], c["token_base"], scales=q.scales)
+
+
+def test_framewise_restore_peak_at_most_tenth_of_chunkwise():
+    q, _ = _q(dict(kind="synthetic", T=10_000, L=3, H=4, D=16, s=0.9, seed=1, c=0.3,
+                   group_size=64))
+    cfg = L.identity_layout(4, 16)
+    cont = C.pack_chunk(q, cfg, ["R240"], cache_id=b"\x01" * 16)
+    bs, plan = cont.bitstream(0), cont.plan(0)
+    ms, mc = KV.PagedMemory(), KV.PagedMemory()
+    ms.begin_fetch()
+    mc.begin_fetch()
+    s = restore_stream(bs, plan, cfg, ms, batch_frames=plan.F)
+    c = restore_chunk_wise(bs, plan, cfg, mc)
+    assert s["tokens_written"] == c["tokens_written"] == 10_000
+    assert 10 * s["peak_buffer_bytes"] <= c["peak_buffer_bytes"]
+    for tok in np.random.default_rng(2).integers(0, 10_000, size=32):
+        for layer in range(3):
+            assert torch.equal(ms.read(int(tok), layer), mc.read(int(tok), layer))
+
+
+@pytest.mark.parametrize("into_paged", [False, True])
+def test_loopback_fetch_restores_bitexact(tmp_path, into_paged):
+    cid = b"\x11" * 16
+    q, _ = _q(dict(kind="synthetic", T=256, L=6, H=8, D=32, s=0.9, seed=7, c=0.4, group_size=64))
+    cfg = L.identity_layout(8, 32)
+    chunks = []
+    for j in range(2):
+        cont = C.pack_chunk(q.layer_triplet(j), cfg, ["R240", "R1080"], cache_id=cid,
+                            chunk_index=j, token_start=0, layer_triplet_index=j, F=4)
+        (tmp_path / C.container_filename(cid, j)).write_bytes(cont.to_bytes())
+        chunks.append((cid, j))
+    handle = NS.serve(NS.ChunkStore(str(tmp_path)), ("127.0.0.1", 0))
+    got = []
+    mem = KV.PagedMemory(16, dtype=torch.int8) if into_paged else None
+    try:
+        addr = f"127.0.0.1:{handle.address[1]}"
+        tl = FE.live_fetch_pipeline(addr, chunks, None, "fixed:R240", prior_gbps=6.0,
+                                    on_chunk=lambda rec, r: got.append(r), mem=mem)
+    finally:
+        handle.close()
+    assert len(got) == 2 and len(tl.records) == 2
+    assert all(r["decode_end"] is not None for r in tl.records)
+    if into_paged:
+        for t in (0, 100, 255):
+            for l in range(6):
+                assert torch.equal(mem.read(t, l), q.values[t, l].reshape(-1))
+    else:
+        for j, slab in enumerate(got):
+            assert torch.equal(slab.values, q.values[:, 3 * j:3 * j + 3])
+            assert torch.equal(slab.scales, q.scales[3 * j:3 * j + 3])
+
+
+def test_fetch_errors(tmp_path):
+    handle = NS.serve(NS.ChunkStore(str(tmp_path)), ("127.0.0.1", 0))
+    try:
+        addr = f"127.0.0.1:{handle.address[1]}"
+        with pytest.raises(NS.ChunkNotFound):
+            NS.fetch_chunk(addr, b"\x00" * 16, 0, "R240")
+        with pytest.raises(NS.ProtocolError):
+            NS.fetch_chunk(addr, b"\x00" * 16, 0, 7)
+    finally:
+        handle.close()

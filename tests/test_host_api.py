@@ -1,0 +1,123 @@
+"""Host-side logic of the drop-in API (no GPU): frame plans, container format,
+wire protocol, resolution selection — against the reference's hand oracles
+(tests/test_layout.py:91-139, tests/test_container.py:66-164,
+tests/test_acceptance.py:265-299) and the pinned oracle."""
+
+import struct
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import ref
+from paper_2602_09725_b200 import container as C
+from paper_2602_09725_b200 import fetch as FE
+from paper_2602_09725_b200 import layout as L
+from paper_2602_09725_b200 import netstore as NS
+
+
+def test_placement_small_plan_by_hand():
+    plan = L.FramePlan(10, 2, L.identity_layout(2, 2), F=2)
+    expected = {0: (0, 0, 0), 1: (1, 0, 0), 2: (0, 0, 1), 3: (1, 0, 1), 4: (2, 0, 0),
+                5: (3, 0, 0), 6: (2, 0, 1), 7: (3, 0, 1), 8: (4, 0, 0), 9: (5, 0, 0)}
+    for i, want in expected.items():
+        assert plan.placement(i) == want
+    assert plan.frame_count == 6
+    assert plan.frame_slots(4) == [(8, 0, 0)]
+    with pytest.raises(ValueError):
+        plan.placement(10)
+
+
+def test_plans_match_oracle_and_digests(golden):
+    for c in golden["frames"]:
+        plan = L.plan_inter_frame(c["T"], c["res"], L.LayoutConfig(*c["layout"]), c["F"])
+        assert plan.frame_shape() == tuple(c["shape"])
+        assert plan.digest() == c["digest"]
+        op = ref.Plan(c["T"], c["res"], *c["layout"], F=c["F"])
+        for i in range(0, c["T"], max(1, c["T"] // 37)):
+            assert plan.placement(i) == op.placement(i)
+        for f in range(plan.frame_count):
+            assert plan.frame_slots(f) == op.frame_slots(f)
+
+
+def test_tiling_candidates_and_validation():
+    assert len(L.tiling_candidates(32, 128)) == 48
+    assert len({c.key() for c in L.tiling_candidates(32, 128)}) == 48
+    with pytest.raises(ValueError):
+        L.LayoutConfig(12, 64, 3, 4, 8, 8)
+    with pytest.raises(ValueError):
+        L.LayoutConfig(16, 64, 2, 4, 8, 8)
+    cfg = L.LayoutConfig(16, 64, 4, 4, 8, 8)
+    assert L.LayoutConfig.from_json(cfg.to_json()) == cfg
+
+
+def _container(seed):
+    rng = np.random.default_rng(seed)
+    codes = sorted(rng.choice(4, size=int(rng.integers(1, 5)), replace=False).tolist())
+    payloads = {c: rng.integers(0, 256, size=int(rng.integers(0, 300))).astype(np.uint8).tobytes()
+                for c in codes}
+    meta = {"layout": L.identity_layout(4, 8).to_json(), "F": 4, "plans": {}, "frame_counts": {},
+            "group_size": 8, "scales_b64": "AACAPw==" * 0 + ""}
+    return C.ChunkContainer(rng.bytes(16), int(rng.integers(0, 2**32)), int(rng.integers(0, 2**32)),
+                            int(rng.integers(1, 10000)), int(rng.integers(0, 256)), meta, payloads)
+
+
+def test_container_round_trips():
+    for seed in range(2000):
+        c = _container(seed)
+        blob = c.to_bytes()
+        back = C.ChunkContainer.from_bytes(blob)
+        assert back.to_bytes() == blob
+        assert back.payloads == c.payloads
+        hdr, entries = C.parse_header(blob)
+        assert [e[0] for e in entries] == c.resolutions
+    with pytest.raises(ValueError):
+        C.parse_header(b"XXXX" + blob[4:])
+    with pytest.raises(ValueError):
+        C.parse_header(blob[:10])
+
+
+def test_container_bytes_layout_matches_oracle(golden):
+    # Same payload bytes -> same container bytes as the oracle's to_bytes restatement.
+    for c in golden["container"]:
+        x = cases.quant_input(c["kv"])
+        v, s = ref.quantize(x, c["kv"]["group_size"])
+        blob = ref.pack_chunk_bytes(v, s, c["layout"], c["res"], c["kv"]["group_size"],
+                                    bytes.fromhex(c["cache_id"]), c["chunk_index"],
+                                    c["token_start"], c["triplet"], c["F"])
+        back = C.ChunkContainer.from_bytes(blob)
+        assert back.to_bytes() == blob
+        assert np.array_equal(back.scales(), s)
+
+
+def test_wire_round_trips():
+    rng = np.random.default_rng(1)
+    for _ in range(5000):
+        req = NS.WireRequest(rng.bytes(16), int(rng.integers(0, 2**32)), int(rng.integers(0, 4)))
+        assert NS.WireRequest.decode(req.encode()) == req
+        resp = NS.WireResponse(int(rng.integers(0, 3)), {"k": int(rng.integers(0, 99))},
+                               rng.bytes(int(rng.integers(0, 64))))
+        back = NS.WireResponse.decode(resp.encode())
+        assert (back.status, back.metadata, back.payload) == (resp.status, resp.metadata, resp.payload)
+    with pytest.raises(NS.ProtocolError):
+        NS.WireRequest.decode(b"\x00" * 5)
+    with pytest.raises(NS.ProtocolError):
+        NS.WireRequest.decode(struct.pack("<4sB16sIB", b"NOPE", 1, b"\0" * 16, 0, 0))
+
+
+def test_select_resolution_and_bandwidth():
+    table = FE.LookupTable("flat", 1, {r: [0.1] for r in L.RESOLUTION_ORDER},
+                           {"R240": 0.05, "R480": 0.05, "R640": 0.05, "R1080": 0.0},
+                           {"R240": 10, "R480": 20, "R640": 30, "R1080": 50})
+    assert FE.estimate_bandwidth([(1e9, 1.0)]) == pytest.approx(8.0)
+    assert FE.estimate_bandwidth([], prior_gbps=3) == 3.0
+    with pytest.raises(RuntimeError):
+        FE.estimate_bandwidth([])
+    for bw in (0.5, 1, 2, 4, 8, 16, 64):
+        got = FE.select_resolution(bw, 1, "R1080", table)
+        deltas = []
+        for r in L.RESOLUTION_ORDER:
+            pen = table.tau_penalty(r) if r != "R1080" else 0.0
+            deltas.append((abs(table.size_bytes(r) * 8 / (bw * 1e9) - 0.1 - pen), r))
+        best = min(d for d, _ in deltas)
+        assert got == [r for d, r in deltas if d == best][-1]
