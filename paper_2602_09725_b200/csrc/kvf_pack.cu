@@ -24,6 +24,8 @@ namespace kvf {
 
 kvf_status launch_pack_coop(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                             cudaStream_t s, bool* launched);
+kvf_status launch_pack_team(const std::vector<kvf_pack_unit>& units, int32_t dtype,
+                            cudaStream_t s, bool* launched);
 
 namespace {
 
@@ -628,7 +630,8 @@ kvf_status launch_fused_group(const std::vector<kvf_pack_unit>& units, int vpl, 
     kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero scratch + counters
     if (st != KVF_OK) return st;
     bool launched = false;
-    st = launch_pack_coop(part, dtype, s, &launched);
+    const char* mode = getenv("KVF_PACK_MODE");
+    if (!(mode && strcmp(mode, "l2") == 0)) st = launch_pack_coop(part, dtype, s, &launched);
     if (st != KVF_OK) return st;
     if (!launched) {
       st = launch_fused_l2(part, vpl, dtype, s);
@@ -636,6 +639,37 @@ kvf_status launch_fused_group(const std::vector<kvf_pack_unit>& units, int vpl, 
     }
   }
   return KVF_OK;
+}
+
+// Zero the scratch, then the team kernel per launch-sized slice of units with
+// one group size; slices it cannot take run the phase-split kernels.
+kvf_status launch_team_group(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+                             cudaStream_t s) {
+  constexpr size_t kChunk = 88;  // units per team launch (kMaxTeamUnits)
+  std::vector<kvf_pack_unit> rest;
+  std::vector<std::vector<kvf_pack_unit>> by_gs;
+  for (const auto& u : units) {
+    bool placed = false;
+    for (auto& b : by_gs)
+      if (b[0].plan.group_size == u.plan.group_size) {
+        b.push_back(u);
+        placed = true;
+        break;
+      }
+    if (!placed) by_gs.push_back({u});
+  }
+  for (const auto& b : by_gs)
+    for (size_t at = 0; at < b.size(); at += kChunk) {
+      size_t n = std::min(kChunk, b.size() - at);
+      std::vector<kvf_pack_unit> part(b.begin() + at, b.begin() + at + n);
+      kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero maxima + counters
+      if (st != KVF_OK) return st;
+      bool launched = false;
+      st = launch_pack_team(part, dtype, s, &launched);
+      if (st != KVF_OK) return st;
+      if (!launched) rest.insert(rest.end(), part.begin(), part.end());
+    }
+  return rest.empty() ? KVF_OK : launch_phases(rest, vpl, dtype, 2 | 4 | 8, s);
 }
 
 kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, cudaStream_t s) {
@@ -649,13 +683,23 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, cudaStre
   for (int v = 0; v <= 16; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        // Default: the two-pass kernels (fastest measured); the
-        // single-read fused schedules are opt-in: KVF_PACK_MODE=fused.
+        // Default: the phase-split kernels (absmax pass, then quantise pass;
+        // fastest measured).  KVF_PACK_MODE=team selects the
+        // single-HBM-read team kernel (kvf_pack_team.cu), =fused|l2 the
+        // cooperative / L2-reuse schedules — all slower on B200.
         const char* mode = getenv("KVF_PACK_MODE");
-        const bool fused = v != 0 && dt != KVF_I8 && phases == (1 | 2 | 4 | 8) && mode &&
-                           strcmp(mode, "fused") == 0;
-        kvf_status st = fused ? launch_fused_group(groups[v][dt], v, dt, s)
-                              : launch_phases(groups[v][dt], v, dt, phases, s);
+        const bool whole = v != 0 && dt != KVF_I8 && phases == (1 | 2 | 4 | 8);
+        const bool fused = whole && mode &&
+                           (strcmp(mode, "fused") == 0 || strcmp(mode, "l2") == 0);
+        const bool team = whole && mode && strcmp(mode, "team") == 0;
+        kvf_status st = KVF_OK;
+        if (fused) {
+          st = launch_fused_group(groups[v][dt], v, dt, s);
+        } else if (team) {
+          st = launch_team_group(groups[v][dt], v, dt, s);
+        } else {
+          st = launch_phases(groups[v][dt], v, dt, phases, s);
+        }
         if (st != KVF_OK) return st;
       }
   return KVF_OK;

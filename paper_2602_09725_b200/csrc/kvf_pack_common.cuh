@@ -15,10 +15,15 @@ constexpr int kPackWarps = kPackThreads / 32;
 constexpr int kMaxPackUnits = 96;  // descriptors per launch (kernel params <= 32 KB)
 
 // Scratch words of a unit (kvf_pack_scratch_words): [3, G] maxima | 3 per-plane
-// done counters | 1 queue word | 3 * (C/256) per-stripe counters.
-inline int64_t pack_scratch_words(const kvf_plan& p) {
+// done counters | 1 queue word | 3 * (C/256) per-stripe counters | [3, G]
+// per-(plane, group) team counters.
+inline int64_t pack_stripe_words(const kvf_plan& p) {
   const int64_t C = (int64_t)p.H * p.D;
-  return 3 * (C / p.group_size) + 4 + 3 * (C >= 256 ? C / 256 : 1);
+  return 3 * (C >= 256 ? C / 256 : 1);
+}
+inline int64_t pack_scratch_words(const kvf_plan& p) {
+  const int64_t G = (int64_t)p.H * p.D / p.group_size;
+  return 3 * G + 4 + pack_stripe_words(p) + 3 * G;
 }
 
 struct PackUnitDev {
@@ -27,6 +32,7 @@ struct PackUnitDev {
   uint32_t* absmax;       // [3, G] maxima (f32 bit patterns)
   uint32_t* done;         // absmax + 3G: per-plane counters, then the queue word
   uint32_t* stripe_done;  // absmax + 3G + 4: per-(plane, stripe) counters
+  uint32_t* team_done;    // then [3, G] per-(plane, group) team counters
   float* scales;
   kvf_surface fr;
   FastDiv div_bs;
@@ -43,6 +49,7 @@ inline PackUnitDev make_pack_unit_dev(const kvf_pack_unit& u) {
   d.absmax = u.absmax;
   d.done = u.absmax ? u.absmax + 3 * d.G : nullptr;
   d.stripe_done = u.absmax ? u.absmax + 3 * d.G + 4 : nullptr;
+  d.team_done = u.absmax ? d.stripe_done + pack_stripe_words(u.plan) : nullptr;
   d.n_scratch = (int32_t)pack_scratch_words(u.plan);
   d.scales = u.scales;
   d.fr = u.frames;

@@ -92,13 +92,15 @@ def _pack_unit(kv_dev, lay, res, T0, T, F, gs, frames, absmax, scales, triplet=0
 @pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
                                  (8, 128, 2, 4, 16, 8), (4, 64, 1, 4, 64, 1)])
 @pytest.mark.parametrize("res", ["R240", "R640", "R1080"])
-def test_fused_pack_matches_oracle(lay, res):
+@pytest.mark.parametrize("mode", ["team", "twopass"])
+def test_fused_pack_matches_oracle(lay, res, mode, monkeypatch):
+    monkeypatch.setenv("KVF_PACK_MODE", mode)  # read by libkvf at each kvf_pack_batch
     H, D = lay[0], lay[1]
     T, Lyr, gs = 700, 5, 128 if D >= 128 else 64
     x = cases.to_bf16_values(ref.gen_synthetic_kv(T, Lyr, H, D, 0.9, 3, 0.3))
     kv = np_bf16_from_f32(x).cuda()
     chunks = [(0, 400), (400, 300)]
-    units, outs = [], []
+    units, outs, scratch = [], [], []
     for trip in range(2):
         for T0, Tc in chunks:
             plan = L.plan_inter_frame(Tc, res, L.LayoutConfig(*lay), 4)
@@ -109,6 +111,7 @@ def test_fused_pack_matches_oracle(lay, res):
             u, plan = _pack_unit(kv, lay, res, T0, Tc, 4, gs, fr, am, sc, trip)
             units.append(u)
             outs.append((trip, T0, Tc, plan, fr, sc))
+            scratch.append(am)  # descriptors hold raw pointers: keep the buffers alive
     arr = (_lib.kvf_pack_unit * len(units))(*units)
     _lib.call("kvf_pack_batch", arr, len(units), None)
     torch.cuda.synchronize()
@@ -118,8 +121,55 @@ def test_fused_pack_matches_oracle(lay, res):
         v, s = ref.quantize(slab, gs)
         oplan = ref.Plan(Tc, res, *lay, F=4)
         want = ref.assemble_frames(v.reshape(Tc, 3, H * D), oplan)
-        assert np.array_equal(sc.cpu().numpy(), s)
-        assert np.array_equal(fr.cpu().numpy(), want)
+        np.testing.assert_array_equal(sc.cpu().numpy(), s, err_msg=f"scales trip {trip} T0 {T0}")
+        np.testing.assert_array_equal(fr.cpu().numpy(), want, err_msg=f"frames trip {trip} T0 {T0}")
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("mode", ["team", "twopass"])
+def test_pack_paged_source_dtypes(dtype, mode, monkeypatch):
+    """Pack from a paged [blocks, 16, H, D] cache through a shuffled block table
+    (vLLM layout) for every source dtype; codes, scales, frames vs the oracle."""
+    monkeypatch.setenv("KVF_PACK_MODE", mode)
+    H, D, gs, bs, T, res = 8, 128, 128, 16, 1234, "R480"
+    lay = (H, D, 1, H, 1, D)
+    x = ref.gen_synthetic_kv(T, 3, H, D, 0.9, 11, 0.3)
+    xt = torch.from_numpy(x).to(dtype)
+    x = xt.float().numpy()                         # the values the kernel sees
+    nblk = (T + bs - 1) // bs
+    perm = torch.randperm(nblk + 7, generator=torch.Generator().manual_seed(5))[:nblk]
+    pool = torch.zeros((3, nblk + 7, bs, H, D), dtype=dtype)
+    tok = torch.arange(T)
+    for p in range(3):
+        pool[p].view(-1, H, D)[perm[tok // bs] * bs + tok % bs] = xt[:, p]
+    pool = pool.cuda()
+    table = perm.to(torch.int32).cuda()
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+    fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
+    am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)), dtype=torch.int32,
+                     device="cuda")
+    sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
+    u = _lib.kvf_pack_unit()
+    for p in range(3):
+        u.src.layer[p] = pool[p].data_ptr()
+    u.src.block_table = table.data_ptr()
+    u.src.block_size = bs
+    u.src.dtype = {torch.bfloat16: 0, torch.float16: 1, torch.float32: 2}[dtype]
+    u.src.block_stride = bs * H * D
+    u.src.slot_stride = H * D
+    u.src.head_stride = D
+    u.src.token_base = 0
+    u.plan = plan.to_c(gs)
+    u.absmax = am.data_ptr()
+    u.scales = sc.data_ptr()
+    from paper_2602_09725_b200 import _dev
+    u.frames = _dev.surface_of(fr)
+    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
+    torch.cuda.synchronize()
+    v, s = ref.quantize(x, gs)
+    want = ref.assemble_frames(v.reshape(T, 3, H * D), ref.Plan(T, res, *lay, F=4))
+    assert np.array_equal(sc.cpu().numpy(), s)
+    assert np.array_equal(fr.cpu().numpy(), want)
 
 
 # ------------------------------------------------------------------ restore
