@@ -54,8 +54,13 @@ def parse():
     ap.add_argument("--layout", default="identity", choices=sorted(LAYOUTS))
     ap.add_argument("--res", default="R1080")
     ap.add_argument("--page", type=int, default=16)
+    ap.add_argument("--requests", type=int, default=0,
+                    help="contexts in the job (default: one per GPU -> weak scaling)")
+    ap.add_argument("--shard", default="layer", choices=["balanced", "layer", "chunk"],
+                    help="unit -> GPU assignment policy (paper_2602_09725_b200/shard.py)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fetch", action="store_true", help="skip the fetch-to-ready leg")
     ap.add_argument("--cpu-units", type=int, default=2, help="sample units per CPU worker")
     return ap.parse_args()
 
@@ -154,11 +159,19 @@ def chunks_of(T):
 
 
 class Workload:
-    """Frames for every (K/V, triplet, chunk) unit + the paged destination cache."""
+    """Frames for this rank's (request, K/V, triplet, chunk) units + their paged caches.
 
-    def __init__(self, args, device):
+    Units come from shard.enumerate_units over `requests` contexts and are
+    assigned to ranks by shard.assign; a rank builds only its own units.  Per
+    owned (request, K/V, triplet) it generates a synthetic [T, 3, H, D] bf16
+    slab on the GPU (AR(1) law of gen_synthetic_kv), packs its chunks into
+    frames with our pack kernels, and allocates the destination paged cache
+    [3, blocks, block_size, H, D] (shuffled block table).
+    """
+
+    def __init__(self, args, device, rank=0, world=1):
         import torch
-        from paper_2602_09725_b200 import _dev, _lib, kvmodel as KV, layout as L
+        from paper_2602_09725_b200 import _dev, _lib, kvmodel as KV, layout as L, shard
         from paper_2602_09725_b200.restore import make_restore_unit
 
         self.torch = torch
@@ -167,60 +180,63 @@ class Workload:
         self.gs = 128
         lay = L.LayoutConfig(H, D, *LAYOUTS[args.layout](H, D))
         self.lay = lay
-        trip = (Lyr + 2) // 3
         bs = args.page
         nblk = (self.T + bs - 1) // bs
         g = torch.Generator(device="cpu")
         g.manual_seed(1234)
         self.table = torch.randperm(nblk + 64, generator=g)[:nblk].to(torch.int32).to(device)
+        all_units = shard.enumerate_units(self.T, Lyr, requests=args.requests or world,
+                                          chunk_tokens=CHUNK)
+        self.all_units = len(all_units)
+        self.mine = shard.units_for_rank(all_units, rank, world, args.shard, H, D)
         self.pack_units, self.units, self.frames, self.scales = [], [], [], []
-        self.caches = []
-        self.elems = 0
-        for kv_i in range(2):  # K then V (seeds 0, 1 as in BASELINE.md)
-            kv = KV.gen_synthetic_kv(self.T, Lyr, H, D, 0.9, seed=kv_i, channel_smoothness=0.3,
-                                     dtype=torch.bfloat16).data
-            cache = torch.empty((Lyr, nblk + 64, bs, H, D), dtype=torch.bfloat16, device=device)
+        self.caches, self._keep = [], []
+        self.elems = sum(u.elements(H, D) for u in self.mine)
+        keys = sorted({(u.request, u.kv, u.triplet) for u in self.mine})
+        for (r, kv_i, j) in keys:
+            real = min(3, Lyr - 3 * j)
+            seed = (r * 2 + kv_i) * 1000 + j
+            slab = KV.gen_synthetic_kv(self.T, real, H, D, 0.9, seed=seed, channel_smoothness=0.3,
+                                       dtype=torch.bfloat16).data
+            cache = torch.empty((real, nblk + 64, bs, H, D), dtype=torch.bfloat16, device=device)
+            self._keep += [slab]
             self.caches.append(cache)
-            for j in range(trip):
-                for (t0, tc) in chunks_of(self.T):
-                    plan = L.plan_inter_frame(tc, args.res, lay, 4)
-                    fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device=device)
-                    am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(self.gs)),
-                                     dtype=torch.int32, device=device)
-                    sc = torch.empty((3, H * D // self.gs), dtype=torch.float32, device=device)
-                    src = _lib.kvf_paged()
-                    dst = _lib.kvf_paged()
-                    for p in range(3):
-                        l = 3 * j + p
-                        src.layer[p] = kv[:, l].data_ptr() if l < Lyr else None
-                        dst.layer[p] = cache[l].data_ptr() if l < Lyr else None
-                        if l < Lyr:
-                            self.elems += tc * H * D
-                    src.block_table = None
-                    src.block_size = 1
-                    src.dtype = _lib.KVF_BF16
-                    src.block_stride = src.slot_stride = Lyr * H * D
-                    src.head_stride = D
-                    src.token_base = t0
-                    dst.block_table = self.table.data_ptr()
-                    dst.block_size = bs
-                    dst.dtype = _lib.KVF_BF16
-                    dst.block_stride = bs * H * D
-                    dst.slot_stride = H * D
-                    dst.head_stride = D
-                    dst.token_base = t0
-                    pu = _lib.kvf_pack_unit()
-                    pu.src = src
-                    pu.plan = plan.to_c(self.gs)
-                    pu.absmax = am.data_ptr()
-                    pu.scales = sc.data_ptr()
-                    pu.frames = _dev.surface_of(fr)
-                    self.pack_units.append(pu)
-                    self.units.append(make_restore_unit(fr, plan, sc, dst, self.gs))
-                    self.frames.append(fr)
-                    self.scales.append(sc)
-                    self._keep = getattr(self, "_keep", []) + [am]
-            self.kv_src = getattr(self, "kv_src", []) + [kv]
+            for u in (u for u in self.mine if (u.request, u.kv, u.triplet) == (r, kv_i, j)):
+                t0, tc = u.token_start, u.tokens
+                plan = L.plan_inter_frame(tc, args.res, lay, 4)
+                fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device=device)
+                am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(self.gs)),
+                                 dtype=torch.int32, device=device)
+                sc = torch.empty((3, H * D // self.gs), dtype=torch.float32, device=device)
+                src = _lib.kvf_paged()
+                dst = _lib.kvf_paged()
+                for p in range(3):
+                    src.layer[p] = slab[:, p].data_ptr() if p < real else None
+                    dst.layer[p] = cache[p].data_ptr() if p < real else None
+                src.block_table = None
+                src.block_size = 1
+                src.dtype = _lib.KVF_BF16
+                src.block_stride = src.slot_stride = real * H * D
+                src.head_stride = D
+                src.token_base = t0
+                dst.block_table = self.table.data_ptr()
+                dst.block_size = bs
+                dst.dtype = _lib.KVF_BF16
+                dst.block_stride = bs * H * D
+                dst.slot_stride = H * D
+                dst.head_stride = D
+                dst.token_base = t0
+                pu = _lib.kvf_pack_unit()
+                pu.src = src
+                pu.plan = plan.to_c(self.gs)
+                pu.absmax = am.data_ptr()
+                pu.scales = sc.data_ptr()
+                pu.frames = _dev.surface_of(fr)
+                self.pack_units.append(pu)
+                self.units.append(make_restore_unit(fr, plan, sc, dst, self.gs))
+                self.frames.append(fr)
+                self.scales.append(sc)
+                self._keep.append(am)
         self.frame_bytes = sum(f.numel() for f in self.frames)
         self._pack_arr = (_lib.kvf_pack_unit * len(self.pack_units))(*self.pack_units)
         self._restore_arr = (_lib.kvf_restore_unit * len(self.units))(*self.units)
@@ -315,6 +331,51 @@ def e2e_restore(w, steps, torch):
     return ms, w.frame_bytes, out_host.numel() * 2
 
 
+def fetch_to_ready(w, steps, torch):
+    """Fetch-to-ready of the whole context from coded KVFC streams in pinned host
+    memory (what a fetch receives): per step one H2D of every stream's bytes,
+    GPU entropy decode + reconstruction of all 88 units (codec.decode_batch: 2
+    launches), then the batched restore into the paged cache.  Wall clock,
+    host work included; the network leg is modelled from the coded bytes."""
+    from paper_2602_09725_b200 import _lib, codec
+    t0 = time.perf_counter()
+    streams = [bs.data for bs in codec.encode_batch(w.frames, [4] * len(w.frames))]
+    enc_s = time.perf_counter() - t0
+    coded = sum(len(b) for b in streams)
+    indices = [codec.StreamIndex(b) for b in streams]
+    frames, _ = codec.decode_batch(streams, indices=indices)
+    ok = all(torch.equal(a, b) for a, b in zip(frames, w.frames))
+    units = []
+    for u, fr in zip(w.units, frames):
+        nu = _lib.kvf_restore_unit()
+        ctypes_copy(nu, u)
+        nu.frames.base = fr.data_ptr()
+        units.append(nu)
+    arr = (_lib.kvf_restore_unit * len(units))(*units)
+    stream = torch.cuda.current_stream()
+
+    def step(idx):
+        out, _ = codec.decode_batch(streams, out=frames, indices=idx)
+        _lib.call("kvf_restore_batch", arr, len(units), w._dev.stream_ptr(stream))
+        torch.cuda.synchronize()
+
+    step(indices)
+    times, scan = [], []
+    for _ in range(steps):
+        t1 = time.perf_counter()
+        idx = [codec.StreamIndex(b) for b in streams]   # host stream walk, per fetch
+        t2 = time.perf_counter()
+        step(idx)
+        times.append((time.perf_counter() - t1) * 1e3)
+        scan.append((t2 - t1) * 1e3)
+    ms = statistics.median(times)
+    return {"ms": round(ms, 2), "scan_ms": round(statistics.median(scan), 2),
+            "coded_bytes": coded, "frame_bytes": w.frame_bytes,
+            "ratio_int8_over_coded": round(w.frame_bytes / coded, 3),
+            "decode_bitexact": ok, "encode_s": round(enc_s, 2),
+            "link_s": {f"{g}gbps": round(coded * 8 / (g * 1e9), 3) for g in (10, 25, 100)}}
+
+
 def ctypes_copy(dst, src):
     import ctypes
     ctypes.memmove(ctypes.addressof(dst), ctypes.addressof(src), ctypes.sizeof(src))
@@ -349,7 +410,7 @@ def run_reference(args, rank, world):
         "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * wall / len(times), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16",
-        "data": "synthetic", "config": workload_config(args),
+        "data": "synthetic", "config": workload_config(args, world),
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": f"{cores} processes x 1 unit of {CHUNK} tokens x 3 layers "
                                    f"({args.model} shape, {args.layout}, {args.res}) per step"},
@@ -359,14 +420,18 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args):
+def workload_config(args, world=1):
     Lyr, H, D = MODELS[args.model]
-    return {"workload": f"{args.model}-shaped K+V, {args.tokens} tokens, {Lyr} layers "
-                        f"(+pad to x3), {H} KV heads, d={D}: frames -> bf16 paged KV restore",
-            "model_shape": args.model, "tokens": args.tokens, "layout": args.layout,
-            "resolution": args.res, "chunk_tokens": CHUNK, "group_size": 128, "F": 4,
-            "block_size": args.page, "parallelism": f"dp{args.gpus} (units sharded, no collective)",
-            "l2": "inputs larger than L2 (2.1 GB frames + 4.3 GB output per step)"}
+    req = args.requests or world
+    return {"workload": f"{req} x {args.model}-shaped K+V context(s), {args.tokens} tokens, "
+                        f"{Lyr} layers (+pad to x3), {H} KV heads, d={D}: frames -> bf16 paged "
+                        f"KV restore",
+            "model_shape": args.model, "tokens": args.tokens, "requests": req,
+            "layout": args.layout, "resolution": args.res, "chunk_tokens": CHUNK,
+            "group_size": 128, "F": 4, "block_size": args.page,
+            "parallelism": f"dp{world}: (request, K/V, triplet, chunk) units sharded "
+                           f"'{args.shard}' across GPUs, no data-path collective",
+            "l2": "inputs larger than L2 (2.3 GB frames in + 4.3 GB out per GPU per step)"}
 
 
 def main():
@@ -380,25 +445,24 @@ def main():
     import torch
     import torch.distributed as dist
 
+    from paper_2602_09725_b200 import shard
+
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     d = dist if world > 1 else None
 
-    w = Workload(args, dev)
+    w = Workload(args, dev, rank, world)
     stream = torch.cuda.Stream()
     # pack (secondary): frames for the restore steps come from here
     pack_ms, pack_per = time_device(w.pack, stream, max(3, args.steps // 2), args.warmup, torch, d)
     pack_ms /= max(3, args.steps // 2)
     with ClockSampler(local) as clk:
         total_ms, per = time_device(w.restore, stream, args.steps, args.warmup, torch, d)
-    ms = total_ms / args.steps
-    if world > 1:
-        t = torch.tensor([ms, pack_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, pack_ms = t.tolist()
-    elems_total = w.elems * world
+    ms = shard.max_over_ranks(total_ms / args.steps, d, dev)
+    pack_ms = shard.max_over_ranks(pack_ms, d, dev)
+    elems_total = int(shard.sum_over_ranks(w.elems, d, dev))
     value = 2.0 * elems_total / (ms * 1e-3) / 1e9
     peak, peak_kind = load_peaks()
     achieved = 3.0 * w.elems / (ms * 1e-3) / 1e9  # per GPU, algorithmic bytes
@@ -407,15 +471,16 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e_ms, h2d, d2h = e2e_restore(w, max(3, args.steps // 4), torch)
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = t.item()
+        e2e_ms = shard.max_over_ranks(e2e_ms, d, dev)
         e2e = {"value": round(2.0 * elems_total / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(e2e_ms, 3),
                "path": "pinned host frames -> H2D (copy stream) overlapped with per-unit "
                        "kvf_restore_batch (compute stream) -> 2 KB D2H"}
+
+    fetch = None
+    if not args.no_fetch:
+        fetch = fetch_to_ready(w, 3, torch)
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -436,7 +501,7 @@ def main():
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16", "data": "synthetic",
-            "config": workload_config(args),
+            "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                          "peak_kind": peak_kind,
@@ -444,13 +509,14 @@ def main():
                          "algorithmic_bytes_per_step": 3 * w.elems},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "fetch_to_ready": fetch,
             "gpu_launches": w.n_launch_restore * args.steps,
             "clocks": clocks,
             "pack": {"ms_per_step": round(pack_ms, 4),
                      "achieved_gbs": round(pack_ach, 1), "frac": round(pack_ach / peak, 4),
                      "launches_per_step": w.n_launch_pack},
             "step_ms_min_max": [round(min(per), 4), round(max(per), 4)],
-            "units": len(w.units), "elems_per_gpu": w.elems,
+            "units": w.all_units, "units_rank0": len(w.units), "elems_rank0": w.elems,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -26,9 +26,9 @@ __device__ __forceinline__ uint32_t zig(int r) {
 }
 
 __global__ void resid_kernel(const kvf_resid_plane* __restrict__ planes) {
-  const kvf_resid_plane P = planes[blockIdx.y];
+  const kvf_resid_plane P = planes[blockIdx.x];  // planes on x: up to 2^31 - 1 of them
   const int bw = (P.width + 15) / 16, bh = (P.height + 15) / 16;
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y * blockDim.x + threadIdx.x;
   if (b >= bw * bh) return;
   const int by = b / bw, bx = b - by * bw;
   const int y0 = by * 16, x0 = bx * 16;
@@ -145,7 +145,8 @@ extern "C" kvf_status kvf_kvfc_residuals(const kvf_resid_plane* d_planes, int32_
   if (n_planes < 0 || max_blocks < 0 || (n_planes > 0 && !d_planes))
     KVF_FAIL(KVF_EINVAL, "bad residual plane array");
   if (n_planes == 0 || max_blocks == 0) return KVF_OK;
-  dim3 grid((unsigned)((max_blocks + 127) / 128), (unsigned)n_planes);
+  if ((max_blocks + 127) / 128 > 65535) KVF_FAIL(KVF_EUNSUPPORTED, "plane too large");
+  dim3 grid((unsigned)n_planes, (unsigned)((max_blocks + 127) / 128));
   resid_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_planes);
   KVF_CHECK_CUDA(cudaGetLastError());
   return KVF_OK;

@@ -101,12 +101,23 @@ def units_for_rank(units: list[Unit], rank: int, world: int, policy: str = "bala
     return assign(units, world, policy, H, D)[rank]
 
 
-def max_over_ranks(value: float, dist=None, device=None) -> float:
-    """Max of a per-rank timing over the process group (identity without one)."""
-    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+def _reduce(value: float, op: str, dist=None, device=None) -> float:
+    if dist is None:
+        import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return float(value)
     import torch
     t = torch.tensor([float(value)], dtype=torch.float64,
                      device=device if device is not None else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=getattr(dist.ReduceOp, op))
     return float(t.item())
+
+
+def max_over_ranks(value: float, dist=None, device=None) -> float:
+    """Max of a per-rank timing over the default process group (identity without one)."""
+    return _reduce(value, "MAX", dist, device)
+
+
+def sum_over_ranks(value: float, dist=None, device=None) -> float:
+    """Sum of a per-rank count over the default process group (identity without one)."""
+    return _reduce(value, "SUM", dist, device)
