@@ -180,7 +180,7 @@ class Workload:
         self.gs = 128
         lay = L.LayoutConfig(H, D, *LAYOUTS[args.layout](H, D))
         self.lay = lay
-        bs = args.page
+        bs = self.page = args.page
         nblk = (self.T + bs - 1) // bs
         g = torch.Generator(device="cpu")
         g.manual_seed(1234)
@@ -299,7 +299,10 @@ def e2e_restore(w, steps, torch):
         ctypes_copy(nu, u)
         units.append(nu)
 
-    last = w.caches[1][w.Lyr - 1, int(w.table[0].item())][0].reshape(-1)
+    # the first slot the last unit writes (layer 0 of its triplet) is read back
+    u_last = w.mine[-1]
+    blk = int(w.table[u_last.token_start // w.page].item())
+    last = w.caches[-1][0, blk, u_last.token_start % w.page].reshape(-1)
 
     def step():
         for k, u in enumerate(units):
@@ -342,6 +345,8 @@ def fetch_to_ready(w, steps, torch):
     streams = [bs.data for bs in codec.encode_batch(w.frames, [4] * len(w.frames))]
     enc_s = time.perf_counter() - t0
     coded = sum(len(b) for b in streams)
+    # what a fetch's receive ring holds: the coded bytes in pinned host memory
+    streams = [torch.frombuffer(bytearray(b), dtype=torch.uint8).pin_memory() for b in streams]
     indices = [codec.StreamIndex(b) for b in streams]
     frames, _ = codec.decode_batch(streams, indices=indices)
     ok = all(torch.equal(a, b) for a, b in zip(frames, w.frames))

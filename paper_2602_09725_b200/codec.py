@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import threading
 
 import numpy as np
 import torch
@@ -22,6 +23,19 @@ import torch
 from . import _dev, _lib
 
 BLOCK = 16
+
+
+# numpy twins of the descriptor structs of include/kvf.h (kvf_rc_stream,
+# kvf_recon_plane, kvf_recon_chain): built vectorised, one H2D copy each.
+_RC_DTYPE = np.dtype([("payload", "<u8"), ("len", "<i8"), ("symbols", "<u8"),
+                      ("n_symbols", "<i8")])
+_PLANE_DTYPE = np.dtype([("symbols", "<u8"), ("modes", "<u8"), ("out", "<u8"),
+                         ("out_pitch", "<i8")])
+_CHAIN_DTYPE = np.dtype([("first", "<i4"), ("count", "<i4"), ("height", "<i4"),
+                         ("width", "<i4")])
+assert _RC_DTYPE.itemsize == C.sizeof(_lib.kvf_rc_stream)
+assert _PLANE_DTYPE.itemsize == C.sizeof(_lib.kvf_recon_plane)
+assert _CHAIN_DTYPE.itemsize == C.sizeof(_lib.kvf_recon_chain)
 
 
 class DecodeError(RuntimeError):
@@ -62,15 +76,27 @@ def _as_bytes(bs) -> bytes:
     return bs.data if isinstance(bs, Bitstream) else bytes(bs)
 
 
+def _host_view(bs):
+    """(address, size, keepalive) of a stream's host bytes without copying:
+    bytes / Bitstream, or a CPU uint8 tensor (e.g. a pinned receive buffer)."""
+    if isinstance(bs, torch.Tensor):
+        if bs.is_cuda or bs.dtype != torch.uint8 or not bs.is_contiguous():
+            raise ValueError("tensor streams must be contiguous CPU uint8 tensors")
+        return bs.data_ptr(), bs.numel(), bs
+    data = _as_bytes(bs)
+    return (C.cast(C.c_char_p(data), C.c_void_p).value or 0), len(data), data
+
+
 class StreamIndex:
     """Layout of one KVFC stream (host arrays from kvf_kvfc_scan)."""
 
-    def __init__(self, data: bytes):
+    def __init__(self, data):
         lib = _lib.load()
         info = _lib.kvf_kvfc_info()
         bad = C.c_int32(0)
-        buf = C.c_char_p(data) if data else None
-        st = lib.kvf_kvfc_scan(buf, len(data), C.byref(info), None, None, None, None, 0,
+        addr, size, _keep = _host_view(data)
+        buf = C.c_void_p(addr) if size else None
+        st = lib.kvf_kvfc_scan(buf, size, C.byref(info), None, None, None, None, 0,
                                C.byref(bad))
         if st == _lib.KVF_EDECODE:
             raise DecodeError(lib.kvf_last_error().decode(), frame_index=bad.value)
@@ -80,13 +106,43 @@ class StreamIndex:
         self.payload_len = np.zeros(3 * n, np.int32)
         self.bitmap_off = np.zeros(3 * n, np.int64)
         self.frame_type = np.zeros(max(n, 1), np.uint8)
-        st = lib.kvf_kvfc_scan(buf, len(data), C.byref(info),
+        st = lib.kvf_kvfc_scan(buf, size, C.byref(info),
                                self.payload_off.ctypes.data, self.payload_len.ctypes.data,
                                self.bitmap_off.ctypes.data, self.frame_type.ctypes.data, n,
                                C.byref(bad))
         if st == _lib.KVF_EDECODE:
             raise DecodeError(lib.kvf_last_error().decode(), frame_index=bad.value)
         _lib.check(st)
+
+
+class _PinnedStaging:
+    """Grow-only pinned host buffer for the coded bytes of a decode batch.
+
+    Pinning a fresh buffer per call costs ~0.1 s/GB; this one is reused.  A
+    buffer is handed out only after the H2D copy that last read it completed
+    (event recorded on the copying stream), so reuse never races a copy.
+    """
+
+    def __init__(self):
+        self._buf = None
+        self._done = None
+        self._lock = threading.Lock()
+
+    def acquire(self, nbytes: int) -> torch.Tensor:
+        self._lock.acquire()
+        if self._done is not None:
+            self._done.synchronize()
+        if self._buf is None or self._buf.numel() < nbytes:
+            self._buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        return self._buf[:nbytes]
+
+    def release(self, stream) -> None:
+        self._done = torch.cuda.Event()
+        self._done.record(stream)
+        self._lock.release()
+
+
+_STAGING = _PinnedStaging()
 
 
 def _to_device_struct_array(arr, device) -> torch.Tensor:
@@ -97,7 +153,9 @@ def _to_device_struct_array(arr, device) -> torch.Tensor:
 def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     """Decode many KVFC streams on the GPU in one pair of launches.
 
-    ``streams``: list of bytes / Bitstream.  ``out``: optional list of
+    ``streams``: list of bytes / Bitstream (staged through a reused pinned
+    buffer), or of contiguous CPU uint8 tensors — pinned receive buffers —
+    which are copied to the device directly.  ``out``: optional list of
     [n, 3, h, w] uint8 CUDA tensors (any row pitch) to decode into.
     ``ranges``: optional per-stream (first, stop) frame range; ``first`` must
     be an intra frame (a chain start), and the output holds stop-first frames.
@@ -105,7 +163,8 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     reference.
     """
     dev = _dev.device()
-    datas = [_as_bytes(s) for s in streams]
+    pinned_in = all(isinstance(x, torch.Tensor) for x in streams) and len(streams) > 0
+    datas = list(streams) if pinned_in else [_as_bytes(x) for x in streams]
     idxs = indices if indices is not None else [StreamIndex(d) for d in datas]
     if ranges is None:
         ranges = [(0, ix.n) for ix in idxs]
@@ -126,26 +185,33 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
                       int((ix.payload_off[ks] + ix.payload_len[ks]).max())))
     sizes = [hi - lo for lo, hi in spans]
     starts = np.cumsum([0] + sizes)
-    host = torch.empty(int(starts[-1]) or 1, dtype=torch.uint8, pin_memory=True)
-    hv = host.numpy()
-    for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
-        hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    if pinned_in:  # receive buffers already in (pinned) host memory: H2D each span
+        with torch.cuda.stream(s):
+            blob = torch.empty(int(starts[-1]) or 1, dtype=torch.uint8, device=dev)
+            for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
+                if hi > lo:
+                    blob[s0:s0 + hi - lo].copy_(d[lo:hi], non_blocking=True)
+    else:
+        host = _STAGING.acquire(int(starts[-1]) or 1)
+        hv = host.numpy()
+        for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
+            hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
+        with torch.cuda.stream(s):
+            blob = host.to(dev, non_blocking=True)
+            _STAGING.release(s)
     # shift so that stream offsets index the copied span
     starts = starts - np.array([lo for lo, _ in spans] + [0])
-    s = stream if stream is not None else torch.cuda.current_stream()
     with torch.cuda.stream(s):
-        blob = host.to(dev, non_blocking=True)
         frames = []
         n_fr = [f1 - f0 for f0, f1 in ranges]
         n_sym = sum(3 * nf * ix.h * ix.w for nf, ix in zip(n_fr, idxs))
         symbols = torch.empty(max(n_sym, 1), dtype=torch.uint8, device=dev)
-        rc = (_lib.kvf_rc_stream * max(1, 3 * sum(n_fr)))()
-        planes = (_lib.kvf_recon_plane * max(1, 3 * sum(n_fr)))()
-        chains = []
-        k_rc = 0
-        sym_at = 0
         base = blob.data_ptr()
         sym_base = symbols.data_ptr()
+        rc_parts, plane_parts, chain_parts = [], [], []
+        sym_at = 0
+        n_planes = 0
         for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
             nf = f1 - f0
             fr = out[j] if out is not None else torch.empty((nf, 3, ix.h, ix.w),
@@ -153,50 +219,47 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
             if tuple(fr.shape) != (nf, 3, ix.h, ix.w):
                 raise ValueError("output frames have the wrong shape")
             frames.append(fr)
-            hw = ix.h * ix.w
-            plane_at = k_rc
-            for f in range(f0, f1):
-                for p in range(3):
-                    k = 3 * f + p
-                    e = rc[k_rc]
-                    e.payload = base + int(starts[j] + ix.payload_off[k])
-                    e.len = int(ix.payload_len[k])
-                    e.symbols = sym_base + sym_at
-                    e.n_symbols = hw
-                    q = planes[k_rc]
-                    q.symbols = sym_base + sym_at
-                    q.modes = (base + int(starts[j] + ix.bitmap_off[k])) if ix.bitmap_off[k] >= 0 else None
-                    q.out = fr[f - f0, p].data_ptr()
-                    q.out_pitch = fr.stride(2)
-                    sym_at += hw
-                    k_rc += 1
-            if hw == 0:
+            if nf == 0:
                 continue
-            # chains: runs of frames starting at each intra frame, per plane
-            f = f0
-            while f < f1:
-                g = f + 1
-                while g < f1 and ix.frame_type[g] == 1:
-                    g += 1
-                for p in range(3):
-                    # entries of plane p for frames f..g-1 are strided by 3
-                    chains.append((plane_at, f - f0, g - f0, p, ix.h, ix.w))
-                f = g
-        # re-pack planes so each chain's entries are contiguous
-        flat = (_lib.kvf_recon_plane * max(1, k_rc))()
-        ch_arr = (_lib.kvf_recon_chain * max(1, len(chains)))()
-        at = 0
-        for c, (plane_at, f, g, p, h, w) in enumerate(chains):
-            ch_arr[c].first = at
-            ch_arr[c].count = g - f
-            ch_arr[c].height = h
-            ch_arr[c].width = w
-            for ff in range(f, g):
-                flat[at] = planes[plane_at + 3 * ff + p]
-                at += 1
-        d_rc = _to_device_struct_array(rc, dev)
-        d_planes = _to_device_struct_array(flat, dev)
-        d_chains = _to_device_struct_array(ch_arr, dev)
+            hw = ix.h * ix.w
+            ks = np.arange(3 * f0, 3 * f1)                 # stream k = 3 f + p, frame-major
+            loc = ks - 3 * f0
+            stream_base = base + int(starts[j])
+            rc = np.empty(len(ks), _RC_DTYPE)
+            rc["payload"] = stream_base + ix.payload_off[ks]
+            rc["len"] = ix.payload_len[ks]
+            rc["symbols"] = sym_base + sym_at + loc * hw
+            rc["n_symbols"] = hw
+            pl = np.empty(len(ks), _PLANE_DTYPE)
+            pl["symbols"] = rc["symbols"]
+            pl["modes"] = np.where(ix.bitmap_off[ks] >= 0, stream_base + ix.bitmap_off[ks], 0)
+            pl["out"] = fr.data_ptr() + (loc // 3) * fr.stride(0) + (loc % 3) * fr.stride(1)
+            pl["out_pitch"] = fr.stride(2)
+            rc_parts.append(rc)
+            sym_at += len(ks) * hw
+            if hw:
+                # chains: per plane, the frames from each intra frame to the next
+                # one (a reconstruction dependency chain), contiguous in `flat`
+                f = ks // 3
+                seg = np.cumsum(ix.frame_type[f0:f1] == 0)[f - f0]
+                order = np.lexsort((f, ks % 3, seg))
+                plane_parts.append(pl[order])
+                key = seg[order] * 3 + (ks % 3)[order]
+                first = np.flatnonzero(np.r_[True, key[1:] != key[:-1]])
+                ch = np.empty(len(first), _CHAIN_DTYPE)
+                ch["first"] = n_planes + first
+                ch["count"] = np.diff(np.r_[first, len(order)])
+                ch["height"], ch["width"] = ix.h, ix.w
+                chain_parts.append(ch)
+                n_planes += len(order)
+        rc = np.concatenate(rc_parts) if rc_parts else np.zeros(1, _RC_DTYPE)
+        flat = np.concatenate(plane_parts) if plane_parts else np.zeros(1, _PLANE_DTYPE)
+        ch_arr = np.concatenate(chain_parts) if chain_parts else np.zeros(1, _CHAIN_DTYPE)
+        k_rc = sum(len(x) for x in rc_parts)
+        chains = ch_arr if chain_parts else []
+        d_rc = torch.from_numpy(rc.view(np.uint8)).to(dev)
+        d_planes = torch.from_numpy(flat.view(np.uint8)).to(dev)
+        d_chains = torch.from_numpy(ch_arr.view(np.uint8)).to(dev)
         sp = _dev.stream_ptr(s)
         _lib.call("kvf_rc_decode", _dev.ptr(d_rc), k_rc, sp)
         _lib.call("kvf_kvfc_reconstruct", _dev.ptr(d_planes), _dev.ptr(d_chains), len(chains), sp)

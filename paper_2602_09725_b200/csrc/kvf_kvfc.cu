@@ -3,12 +3,12 @@
 // 1. rc_decode_kernel: the reference's adaptive range decoder
 //    (fk/rangecoder.py:146-189), one thread per (frame, plane) stream — every
 //    stream resets its model and is length-prefixed, so they are independent.
-//    The model lives in shared memory as 256 packed words per thread,
-//      W[i] = fen[i+1] << 16 | freq[i]      (fen = Fenwick tree of freq),
-//    stored [i][thread] so each thread always hits its own bank.  Counts fit
-//    16 bits: freq <= total - 255 and every Fenwick node below the root covers
-//    at most 128 symbols, while total < 2^16 + 32 (fk/rangecoder.py:48-50).
-//    The root node (total) is never read by the search and is not stored.
+//    The per-symbol work is a serial dependency chain, so the kernel is built
+//    for latency: the top four Fenwick levels are registers, the second
+//    division is replaced by multiplies inside the descent, tree updates are
+//    fire-and-forget shared atomics, the halving rebuild is block-parallel,
+//    and payload words are prefetched one word ahead.  The root node (total)
+//    is never read by the search and is not stored.
 // 2. recon_kernel: per-sample prediction (fk/codec.py:131-144) as segmented
 //    prefix sums mod 256.  One CTA per chain of same-plane frames starting at
 //    an intra frame.  A 16-pixel run of a row never crosses a 16x16 block, so a
@@ -29,74 +29,138 @@ constexpr uint32_t kInc = 32;
 constexpr uint32_t kLimit = 1u << 16;
 
 // Sequential byte reader over a device payload; bytes past the end are 0.
-struct ByteReader {
-  const uint8_t* p;
-  int64_t len;
-  int64_t pos;
-  uint32_t word;    // the aligned 4-byte word holding byte `pos`, when cached
-  uintptr_t waddr;  // address of that word (0 = nothing cached)
+// Two aligned words are held: the one being consumed and the next one, whose
+// load is issued four bytes ahead so the dependent decode chain rarely waits.
+struct ByteStream {
+  uintptr_t wa;    // address of the aligned word `cur`
+  uintptr_t end;   // payload end address
+  uint32_t cur, nxt;
+  uint32_t pos, len;
+  const uint8_t* base;
+  __device__ __forceinline__ void init(const uint8_t* p, uint32_t n) {
+    base = p;
+    len = n;
+    pos = 0;
+    end = reinterpret_cast<uintptr_t>(p) + n;
+    wa = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3);
+    cur = n ? __ldg(reinterpret_cast<const uint32_t*>(wa)) : 0u;
+    nxt = wa + 4 < end ? __ldg(reinterpret_cast<const uint32_t*>(wa + 4)) : 0u;
+  }
   __device__ __forceinline__ uint32_t next() {
-    const int64_t i = pos++;
-    if (i >= len) return 0u;
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p + i);
-    const uintptr_t wa = a & ~uintptr_t(3);
-    if (wa != waddr) {
-      word = __ldg(reinterpret_cast<const uint32_t*>(wa));
-      waddr = wa;
+    if (pos >= len) return 0u;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base) + pos++;
+    if ((a & ~uintptr_t(3)) != wa) {  // crossed into the prefetched word
+      wa += 4;
+      cur = nxt;
+      nxt = wa + 4 < end ? __ldg(reinterpret_cast<const uint32_t*>(wa + 4)) : 0u;
     }
-    return (word >> (8 * (a & 3))) & 0xFFu;
+    return (cur >> (8 * (a & 3))) & 0xFFu;
   }
 };
 
-__global__ void __launch_bounds__(224)
+// The reference model (fk/rangecoder.py:53-103): 256 counts, a Fenwick tree of
+// cumulative counts, +INC per coded symbol, halving at TOTAL_LIMIT.  Here the
+// 15 tree nodes that are multiples of 16 (the top four levels of the descent)
+// live in registers R[1..15]; the other nodes and every count live in shared
+// memory as W[i] = fen[i+1] << 16 | freq[i], [i][thread]-major so each thread
+// always hits its own bank.  Counts fit 16 bits: total < 2^16 + 32 and a node
+// below the multiples of 16 covers at most 8 symbols (fk/rangecoder.py:48-50).
+constexpr int kDecThreads = 32;  // one warp per CTA: 32 KB of models, 7 CTAs per SM
+
+__device__ __forceinline__ uint32_t lowbit(uint32_t j) { return j & (0u - j); }
+
+// Halve every count ((f + 1) >> 1, fk/rangecoder.py:93-103) and rebuild the
+// tree block by block (16 symbols per block); returns the new total.
+__device__ __forceinline__ uint32_t rebuild(uint32_t* w, uint32_t (&R)[16]) {
+  uint32_t B[16];
+  uint32_t total = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    uint32_t pre[17];
+    pre[0] = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) pre[q + 1] = pre[q] + (((w[(16 * b + q) * kDecThreads] & 0xFFFFu) + 1) >> 1);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int jl = q + 1;
+      const uint32_t node = pre[jl] - pre[jl - (jl & -jl)];
+      w[(16 * b + q) * kDecThreads] = (node << 16) | (pre[q + 1] - pre[q]);
+    }
+    B[b] = pre[16];
+    total += pre[16];
+  }
+#pragma unroll
+  for (int k = 1; k < 16; ++k) {  // node 16k covers blocks (k - lowbit(k), k]
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = k - (k & -k); b < k; ++b) v += B[b];
+    R[k] = v;
+  }
+  return total;
+}
+
+__global__ void __launch_bounds__(kDecThreads)
     rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n) {
-  extern __shared__ uint32_t W[];  // [256][blockDim.x]
-  const int nt = blockDim.x, tid = threadIdx.x;
-  const int sidx = blockIdx.x * nt + tid;
+  extern __shared__ uint32_t W[];  // [256][kDecThreads]
+  const int tid = threadIdx.x;
+  const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
   const kvf_rc_stream st = streams[sidx];
-#define MW(i) W[(i) * nt + tid]
-  for (int i = 0; i < 256; ++i) {
-    const int j = i + 1;
-    MW(i) = ((uint32_t)(j & -j) << 16) | 1u;  // freq 1, fen[j] = lowbit(j)
-  }
+  uint32_t* w = W + tid;  // word i of this thread's model at w[i * kDecThreads]
+#pragma unroll 8
+  for (int i = 0; i < 256; ++i) w[i * kDecThreads] = (lowbit(i + 1) << 16) | 1u;
+  uint32_t R[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) R[k] = 16u * (uint32_t)(k & -k);
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu, code = 0;
-  ByteReader br{st.payload, st.len, 0, 0u, 0};
-  for (int k = 0; k < 4; ++k) code = (code << 8) | br.next();
+  ByteStream bs;
+  bs.init(st.payload, (uint32_t)st.len);
+  for (int k = 0; k < 4; ++k) code = (code << 8) | bs.next();
 
   uint8_t* out = st.symbols;
+  const uint32_t nsym = (uint32_t)st.n_symbols;
   uint32_t pack = 0;
   const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-  for (int64_t k = 0; k < st.n_symbols; ++k) {
+  for (uint32_t k = 0; k < nsym; ++k) {
     const uint32_t r = rng / total;
-    uint32_t v = (code - low) / r;
-    if (v >= total) v = total - 1;
-    // Fenwick descent: largest s with cum(s) <= v (fk/rangecoder.py:79-90)
-    uint32_t idx = 0, rem = v;
+    // Largest s with cum(s) <= min((code - low) / r, total - 1) (fk/rangecoder.py:163-166,
+    // 79-90), found without the second division: cum <= x / r  <=>  cum * r <= x.
+    const uint32_t x = code - low;
+    uint32_t rem = x, idx = 0, f;
+    f = R[8] * r;
+    if (f <= rem) { rem -= f; idx = 128; }
+    f = (idx ? R[12] : R[4]) * r;
+    if (f <= rem) { rem -= f; idx += 64; }
+    {
+      const uint32_t a = (idx & 128) ? R[10] : R[2], b = (idx & 128) ? R[14] : R[6];
+      f = ((idx & 64) ? b : a) * r;
+      if (f <= rem) { rem -= f; idx += 32; }
+    }
+    {
+      const uint32_t a0 = (idx & 128) ? R[9] : R[1], a1 = (idx & 128) ? R[11] : R[3];
+      const uint32_t a2 = (idx & 128) ? R[13] : R[5], a3 = (idx & 128) ? R[15] : R[7];
+      const uint32_t b0 = (idx & 64) ? a2 : a0, b1 = (idx & 64) ? a3 : a1;
+      f = ((idx & 32) ? b1 : b0) * r;
+      if (f <= rem) { rem -= f; idx += 16; }
+    }
 #pragma unroll
-    for (uint32_t bit = 128; bit; bit >>= 1) {
-      const uint32_t f = MW(idx + bit - 1) >> 16;
-      if (f <= rem) {
-        rem -= f;
-        idx += bit;
-      }
+    for (uint32_t bit = 8; bit; bit >>= 1) {
+      f = (w[(idx + bit - 1) * kDecThreads] >> 16) * r;
+      if (f <= rem) { rem -= f; idx += bit; }
     }
     const uint32_t s = idx;
-    const uint32_t cum = v - rem;
-    const uint32_t fr = MW(s) & 0xFFFFu;
-    low += r * cum;
-    rng = r * fr;
-    for (;;) {
+    low = code - rem;                                   // low + r * cum(s)
+    rng = r * (w[s * kDecThreads] & 0xFFFFu);           // r * freq(s)
+    for (;;) {                                          // fk/rangecoder.py:172-183
       if ((low ^ (low + rng)) >= kTop) {
         if (rng >= kBot) break;
         rng = (0u - low) & (kBot - 1);
       }
-      code = (code << 8) | br.next();
+      code = (code << 8) | bs.next();
       low <<= 8;
       rng <<= 8;
     }
-    // emit (4 symbols per store when aligned)
-    if (aligned4) {
+    if (aligned4) {  // 4 symbols per store
       pack |= s << (8 * (k & 3));
       if ((k & 3) == 3) {
         *reinterpret_cast<uint32_t*>(out + (k - 3)) = pack;
@@ -105,29 +169,34 @@ __global__ void __launch_bounds__(224)
     } else {
       out[k] = (uint8_t)s;
     }
-    // model update: freq[s] += INC and Fenwick path (fk/rangecoder.py:60-66)
-    MW(s) += (kInc << 16) | kInc;
-    for (uint32_t j = (s + 1) + ((s + 1) & (0u - (s + 1))); j <= 255; j += j & (0u - j))
-      MW(j - 1) += kInc << 16;
-    total += kInc;
-    if (total >= kLimit) {  // halve counts, rebuild the tree (fk/rangecoder.py:93-103)
-      total = 0;
-      for (int i = 0; i < 256; ++i) {
-        const uint32_t f = ((MW(i) & 0xFFFFu) + 1) >> 1;
-        total += f;
-        MW(i) = (f << 16) | f;
-      }
-      for (int j = 1; j <= 255; ++j) {
-        const int par = j + (j & -j);
-        if (par <= 255) MW(par - 1) += MW(j - 1) & 0xFFFF0000u;
+    // freq[s] += INC and the Fenwick path of s (fk/rangecoder.py:60-66, 185-186):
+    // shared-memory nodes below the next multiple of 16, then the register nodes.
+    uint32_t j = s + 1;
+    atomicAdd(&w[s * kDecThreads], (j & 15) ? ((kInc << 16) | kInc) : kInc);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // lowbits 1 -> 2 -> 4 -> 8 -> 16: four steps at most
+      if (j & 15) {
+        j += lowbit(j);
+        if (j & 15) atomicAdd(&w[(j - 1) * kDecThreads], kInc << 16);
       }
     }
+    uint32_t kk = j >> 4, mask = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (kk < 16) {
+        mask |= 1u << kk;
+        kk += lowbit(kk);
+      }
+    }
+#pragma unroll
+    for (int q = 1; q < 16; ++q) R[q] += ((mask >> q) & 1u) * kInc;
+    total += kInc;
+    if (total >= kLimit) total = rebuild(w, R);
   }
-  if (aligned4 && (st.n_symbols & 3)) {
-    const int64_t base = st.n_symbols & ~int64_t(3);
-    for (int64_t k = base; k < st.n_symbols; ++k) out[k] = (uint8_t)(pack >> (8 * (k - base)));
+  if (aligned4 && (nsym & 3)) {
+    const uint32_t base = nsym & ~3u;
+    for (uint32_t k = base; k < nsym; ++k) out[k] = (uint8_t)(pack >> (8 * (k - base)));
   }
-#undef MW
 }
 
 // ----------------------------------------------------------- reconstruction
@@ -261,19 +330,12 @@ extern "C" kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_st
                                     void* stream) {
   if (n_streams < 0 || (n_streams > 0 && !d_streams)) KVF_FAIL(KVF_EINVAL, "bad stream array");
   if (n_streams == 0) return KVF_OK;
-  int dev = 0, sms = 0;
-  KVF_CHECK_CUDA(cudaGetDevice(&dev));
-  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // Spread the streams over every SM: threads per CTA = ceil(n / SMs), in
-  // warps, capped by the 224 x 1 KB model footprint per CTA.
-  int per = (n_streams + sms - 1) / sms;
-  per = std::min(224, std::max(32, (per + 31) / 32 * 32));
-  const size_t smem = (size_t)per * 256 * sizeof(uint32_t);
-  KVF_CHECK_CUDA(cudaFuncSetAttribute(rc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(224 * 256 * sizeof(uint32_t))));
-  const int grid = (n_streams + per - 1) / per;
-  rc_decode_kernel<<<grid, per, smem, reinterpret_cast<cudaStream_t>(stream)>>>(d_streams,
-                                                                                n_streams);
+  // One warp per CTA; its 32 models take 32 KB of shared memory, so seven CTAs
+  // (224 streams) are resident per SM and the grid spreads over every SM.
+  const size_t smem = (size_t)kDecThreads * 256 * sizeof(uint32_t);
+  const int grid = (n_streams + kDecThreads - 1) / kDecThreads;
+  rc_decode_kernel<<<grid, kDecThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(d_streams,
+                                                                                      n_streams);
   KVF_CHECK_CUDA(cudaGetLastError());
   return KVF_OK;
 }
