@@ -386,6 +386,23 @@ def ctypes_copy(dst, src):
     ctypes.memmove(ctypes.addressof(dst), ctypes.addressof(src), ctypes.sizeof(src))
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary
+    (profiles/<round>/ncu_traffic.json, written by tools/ncu_summary.py), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")),
+                       reverse=True):
+        try:
+            with open(path) as fh:
+                rec = json.load(fh).get(kernel)
+        except (OSError, ValueError):
+            continue
+        if rec:
+            return {"bytes_per_launch": rec["dram_bytes_per_launch"],
+                    "source": os.path.relpath(path, ROOT) + " (" + rec["report"] + ")"}
+    return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -501,6 +518,9 @@ def main():
 
     if rank == 0:
         clocks = clk.summary()
+        # one restore launch per step covers all 88 units: per-launch traffic
+        # compares with algorithmic_bytes_per_step (multi-GPU: per rank)
+        traffic = ncu_traffic("restore_fast_kernel")
         line = {
             "metric": "KV restore GB/s (frames->bf16 paged KV), 32K ctx",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -508,7 +528,9 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16", "data": "synthetic",
             "config": workload_config(args, world),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic and traffic["bytes_per_launch"],
+                         "traffic_source": traffic and traffic["source"],
                          "peak_kind": peak_kind,
                          "kernel": "restore_fast_kernel (kvf_restore_batch)",
                          "algorithmic_bytes_per_step": 3 * w.elems},

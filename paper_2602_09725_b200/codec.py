@@ -205,7 +205,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     with torch.cuda.stream(s):
         frames = []
         n_fr = [f1 - f0 for f0, f1 in ranges]
-        n_sym = sum(3 * nf * ix.h * ix.w for nf, ix in zip(n_fr, idxs))
+        n_sym = sum(3 * nf * (-(-ix.h * ix.w // 4) * 4) for nf, ix in zip(n_fr, idxs))
         symbols = torch.empty(max(n_sym, 1), dtype=torch.uint8, device=dev)
         base = blob.data_ptr()
         sym_base = symbols.data_ptr()
@@ -222,13 +222,14 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
             if nf == 0:
                 continue
             hw = ix.h * ix.w
+            hw4 = -(-hw // 4) * 4                          # 4-byte aligned symbol slots
             ks = np.arange(3 * f0, 3 * f1)                 # stream k = 3 f + p, frame-major
             loc = ks - 3 * f0
             stream_base = base + int(starts[j])
             rc = np.empty(len(ks), _RC_DTYPE)
             rc["payload"] = stream_base + ix.payload_off[ks]
             rc["len"] = ix.payload_len[ks]
-            rc["symbols"] = sym_base + sym_at + loc * hw
+            rc["symbols"] = sym_base + sym_at + loc * hw4
             rc["n_symbols"] = hw
             pl = np.empty(len(ks), _PLANE_DTYPE)
             pl["symbols"] = rc["symbols"]
@@ -236,7 +237,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
             pl["out"] = fr.data_ptr() + (loc // 3) * fr.stride(0) + (loc % 3) * fr.stride(1)
             pl["out_pitch"] = fr.stride(2)
             rc_parts.append(rc)
-            sym_at += len(ks) * hw
+            sym_at += len(ks) * hw4
             if hw:
                 # chains: per plane, the frames from each intra frame to the next
                 # one (a reconstruction dependency chain), contiguous in `flat`

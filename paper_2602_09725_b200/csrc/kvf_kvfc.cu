@@ -34,27 +34,26 @@ constexpr uint32_t kLimit = 1u << 16;
 struct ByteStream {
   uintptr_t wa;    // address of the aligned word `cur`
   uintptr_t end;   // payload end address
+  uintptr_t a;     // address of the next byte
   uint32_t cur, nxt;
-  uint32_t pos, len;
-  const uint8_t* base;
   __device__ __forceinline__ void init(const uint8_t* p, uint32_t n) {
-    base = p;
-    len = n;
-    pos = 0;
-    end = reinterpret_cast<uintptr_t>(p) + n;
-    wa = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3);
+    a = reinterpret_cast<uintptr_t>(p);
+    end = a + n;
+    wa = a & ~uintptr_t(3);
     cur = n ? __ldg(reinterpret_cast<const uint32_t*>(wa)) : 0u;
     nxt = wa + 4 < end ? __ldg(reinterpret_cast<const uint32_t*>(wa + 4)) : 0u;
   }
+  // Straight-line (predicated) so the per-symbol renormalisation does not
+  // branch: the byte, then the word rotation when `a` crosses into `nxt`.
   __device__ __forceinline__ uint32_t next() {
-    if (pos >= len) return 0u;
-    const uintptr_t a = reinterpret_cast<uintptr_t>(base) + pos++;
-    if ((a & ~uintptr_t(3)) != wa) {  // crossed into the prefetched word
+    const uint32_t b = a < end ? (cur >> (8 * (a & 3))) & 0xFFu : 0u;
+    ++a;
+    if ((a & 3) == 0) {
       wa += 4;
       cur = nxt;
       nxt = wa + 4 < end ? __ldg(reinterpret_cast<const uint32_t*>(wa + 4)) : 0u;
     }
-    return (cur >> (8 * (a & 3))) & 0xFFu;
+    return b;
   }
 };
 
@@ -68,6 +67,7 @@ struct ByteStream {
 constexpr int kDecThreads = 32;  // one warp per CTA: 32 KB of models, 7 CTAs per SM
 
 __device__ __forceinline__ uint32_t lowbit(uint32_t j) { return j & (0u - j); }
+
 
 // Halve every count ((f + 1) >> 1, fk/rangecoder.py:93-103) and rebuild the
 // tree block by block (16 symbols per block); returns the new total.
@@ -121,37 +121,68 @@ __global__ void __launch_bounds__(kDecThreads)
   const uint32_t nsym = (uint32_t)st.n_symbols;
   uint32_t pack = 0;
   const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  double inv = 1.0 / (double)total;  // 1/total of the symbol being decoded
   for (uint32_t k = 0; k < nsym; ++k) {
-    const uint32_t r = rng / total;
+    // r = rng / total (fk/rangecoder.py:163), exact: inv = RN(1/total) has a
+    // relative error <= 2^-53, so rng*inv is within 2^-28 of rng/total, whose
+    // fraction is 0 or in [1/total, 1 - 1/total] with total < 2^16 + 32;
+    // adding 2^-19 before the floor therefore never changes it wrongly.
+    const uint32_t r = __double2uint_rd(__fma_rn((double)rng, inv, 0x1p-19));
+    const double inv_next = 1.0 / (double)(total + kInc);  // off the critical path
     // Largest s with cum(s) <= min((code - low) / r, total - 1) (fk/rangecoder.py:163-166,
     // 79-90), found without the second division: cum <= x / r  <=>  cum * r <= x.
     const uint32_t x = code - low;
-    uint32_t rem = x, idx = 0, f;
+    uint32_t rem = x, f;
+    // top four levels: register nodes 128 | 64,192 | 32..224 | 16..240
     f = R[8] * r;
-    if (f <= rem) { rem -= f; idx = 128; }
-    f = (idx ? R[12] : R[4]) * r;
-    if (f <= rem) { rem -= f; idx += 64; }
+    const bool b7 = f <= rem;
+    if (b7) rem -= f;
+    f = (b7 ? R[12] : R[4]) * r;
+    const bool b6 = f <= rem;
+    if (b6) rem -= f;
     {
-      const uint32_t a = (idx & 128) ? R[10] : R[2], b = (idx & 128) ? R[14] : R[6];
-      f = ((idx & 64) ? b : a) * r;
-      if (f <= rem) { rem -= f; idx += 32; }
+      const uint32_t a = b7 ? R[10] : R[2], b = b7 ? R[14] : R[6];
+      f = (b6 ? b : a) * r;
     }
+    const bool b5 = f <= rem;
+    if (b5) rem -= f;
     {
-      const uint32_t a0 = (idx & 128) ? R[9] : R[1], a1 = (idx & 128) ? R[11] : R[3];
-      const uint32_t a2 = (idx & 128) ? R[13] : R[5], a3 = (idx & 128) ? R[15] : R[7];
-      const uint32_t b0 = (idx & 64) ? a2 : a0, b1 = (idx & 64) ? a3 : a1;
-      f = ((idx & 32) ? b1 : b0) * r;
-      if (f <= rem) { rem -= f; idx += 16; }
+      const uint32_t a0 = b7 ? R[9] : R[1], a1 = b7 ? R[11] : R[3];
+      const uint32_t a2 = b7 ? R[13] : R[5], a3 = b7 ? R[15] : R[7];
+      const uint32_t c0 = b6 ? a2 : a0, c1 = b6 ? a3 : a1;
+      f = (b5 ? c1 : c0) * r;
     }
+    const bool b4 = f <= rem;
+    if (b4) rem -= f;
+    const uint32_t blk = (b7 ? 128u : 0u) + (b6 ? 64u : 0u) + (b5 ? 32u : 0u) + (b4 ? 16u : 0u);
+    // bottom four levels inside the 16-symbol block: all 16 words in one go
+    uint32_t Wb[16];
 #pragma unroll
-    for (uint32_t bit = 8; bit; bit >>= 1) {
-      f = (w[(idx + bit - 1) * kDecThreads] >> 16) * r;
-      if (f <= rem) { rem -= f; idx += bit; }
-    }
-    const uint32_t s = idx;
-    low = code - rem;                                   // low + r * cum(s)
-    rng = r * (w[s * kDecThreads] & 0xFFFFu);           // r * freq(s)
-    for (;;) {                                          // fk/rangecoder.py:172-183
+    for (int q = 0; q < 16; ++q) Wb[q] = w[(blk + q) * kDecThreads];
+    uint32_t F8[8], F4[4], F2[2];  // freq candidates narrowed bit by bit
+    f = (Wb[7] >> 16) * r;
+    const bool b3 = f <= rem;
+    if (b3) rem -= f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) F8[i] = b3 ? Wb[8 + i] : Wb[i];
+    f = (F8[3] >> 16) * r;
+    const bool b2 = f <= rem;
+    if (b2) rem -= f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) F4[i] = b2 ? F8[4 + i] : F8[i];
+    f = (F4[1] >> 16) * r;
+    const bool b1 = f <= rem;
+    if (b1) rem -= f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) F2[i] = b1 ? F4[2 + i] : F4[i];
+    f = (F2[0] >> 16) * r;
+    const bool b0 = f <= rem;
+    if (b0) rem -= f;
+    const uint32_t sl = (b3 ? 8u : 0u) + (b2 ? 4u : 0u) + (b1 ? 2u : 0u) + (b0 ? 1u : 0u);
+    const uint32_t s = blk + sl;
+    low = code - rem;                                      // low + r * cum(s)
+    rng = r * ((b0 ? F2[1] : F2[0]) & 0xFFFFu);            // r * freq(s)
+    for (;;) {                                             // fk/rangecoder.py:172-183
       if ((low ^ (low + rng)) >= kTop) {
         if (rng >= kBot) break;
         rng = (0u - low) & (kBot - 1);
@@ -160,42 +191,43 @@ __global__ void __launch_bounds__(kDecThreads)
       low <<= 8;
       rng <<= 8;
     }
-    if (aligned4) {  // 4 symbols per store
-      pack |= s << (8 * (k & 3));
-      if ((k & 3) == 3) {
+    pack = (pack >> 8) | (s << 24);  // 4 symbols per 32-bit store
+    if ((k & 3) == 3) {
+      if (aligned4) {
         *reinterpret_cast<uint32_t*>(out + (k - 3)) = pack;
-        pack = 0;
-      }
-    } else {
-      out[k] = (uint8_t)s;
-    }
-    // freq[s] += INC and the Fenwick path of s (fk/rangecoder.py:60-66, 185-186):
-    // shared-memory nodes below the next multiple of 16, then the register nodes.
-    uint32_t j = s + 1;
-    atomicAdd(&w[s * kDecThreads], (j & 15) ? ((kInc << 16) | kInc) : kInc);
+      } else {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {  // lowbits 1 -> 2 -> 4 -> 8 -> 16: four steps at most
-      if (j & 15) {
-        j += lowbit(j);
-        if (j & 15) atomicAdd(&w[(j - 1) * kDecThreads], kInc << 16);
+        for (int e = 0; e < 4; ++e) out[k - 3 + e] = (uint8_t)(pack >> (8 * e));
       }
     }
-    uint32_t kk = j >> 4, mask = 0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (kk < 16) {
-        mask |= 1u << kk;
-        kk += lowbit(kk);
-      }
+    // freq[s] += INC and the Fenwick path of s (fk/rangecoder.py:60-66, 185-186),
+    // branch-free: the shared nodes below the block end (at most four: lowbits
+    // 1, 2, 4, 8) as unconditional atomics (+0 when off the path), then every
+    // register node covering s.
+    {
+      const uint32_t j0 = s + 1, j1 = j0 + lowbit(j0), j2 = j1 + lowbit(j1), j3 = j2 + lowbit(j2);
+      const bool p0 = (j0 & 15) != 0, p1 = p0 && (j1 & 15), p2 = p1 && (j2 & 15),
+                 p3 = p2 && (j3 & 15);
+      atomicAdd(&w[s * kDecThreads], p0 ? ((kInc << 16) | kInc) : kInc);
+      atomicAdd(&w[(p1 ? j1 - 1 : s) * kDecThreads], p1 ? kInc << 16 : 0u);
+      atomicAdd(&w[(p2 ? j2 - 1 : s) * kDecThreads], p2 ? kInc << 16 : 0u);
+      atomicAdd(&w[(p3 ? j3 - 1 : s) * kDecThreads], p3 ? kInc << 16 : 0u);
     }
 #pragma unroll
-    for (int q = 1; q < 16; ++q) R[q] += ((mask >> q) & 1u) * kInc;
+    for (int q = 1; q < 16; ++q) {  // node 16q covers s in [16(q - lowbit(q)), 16q)
+      const uint32_t lo = 16u * (uint32_t)(q - (q & -q)), len = 16u * (uint32_t)(q & -q);
+      R[q] += (s - lo < len) ? kInc : 0u;
+    }
     total += kInc;
-    if (total >= kLimit) total = rebuild(w, R);
+    inv = inv_next;
+    if (total >= kLimit) {
+      total = rebuild(w, R);
+      inv = 1.0 / (double)total;
+    }
   }
-  if (aligned4 && (nsym & 3)) {
-    const uint32_t base = nsym & ~3u;
-    for (uint32_t k = base; k < nsym; ++k) out[k] = (uint8_t)(pack >> (8 * (k - base)));
+  if (nsym & 3) {  // tail: the last nsym % 4 symbols sit in the top bytes of `pack`
+    const uint32_t base = nsym & ~3u, n_tail = nsym & 3;
+    for (uint32_t k = base; k < nsym; ++k) out[k] = (uint8_t)(pack >> (8 * (4 - n_tail + k - base)));
   }
 }
 

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import csv
 import io
+import json
 import os
 import subprocess
 import sys
@@ -51,6 +52,7 @@ def report(path, out):
     rows = list(csv.reader(io.StringIO(raw)))
     h, units, vals = rows[0], rows[1], rows[2]
     name = vals[h.index("Kernel Name")] if "Kernel Name" in h else os.path.basename(path)
+    name = name.replace("(anonymous namespace)::", "")
     with open(out, "w") as fh:
         fh.write(f"# ncu --set full: `{name[:120]}`\n\nReport: `{os.path.basename(path)}`\n\n")
         fh.write("| metric | value | unit |\n|---|---|---|\n")
@@ -62,7 +64,16 @@ def report(path, out):
                 v = float(vals[h.index(k)].replace(",", ""))
                 u = units[h.index(k)]
                 return v * {"Gbyte": 1, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9}.get(u, 1)
-            fh.write(f"\nDRAM traffic per launch: {gb('dram__bytes_read.sum') + gb('dram__bytes_write.sum'):.3f} GB\n")
+            traffic = gb('dram__bytes_read.sum') + gb('dram__bytes_write.sum')
+            fh.write(f"\nDRAM traffic per launch: {traffic:.3f} GB\n")
+            # machine-readable: bench.py reports it as roofline.traffic
+            tj = os.path.join(os.path.dirname(out), "ncu_traffic.json")
+            data = json.load(open(tj)) if os.path.exists(tj) else {}
+            short = name.split("(")[0].split("::")[-1].split("<")[0]
+            data[short] = {"dram_bytes_per_launch": traffic * 1e9, "report": os.path.basename(path),
+                           "duration": vals[h.index("gpu__time_duration.sum")] + " "
+                           + units[h.index("gpu__time_duration.sum")]}
+            json.dump(data, open(tj, "w"), indent=1, sort_keys=True)
         stalls = []
         for i, k in enumerate(h):
             if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("_per_issue_active.ratio"):
