@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import codec, container as C, layout as L, netstore as NS
-from .restore import restore_frames
+from .restore import restore_unit, restore_units
 
 MB = 1e6
 GBPS = 1e9
@@ -125,64 +125,153 @@ def _fixed_policy(policy):
     return name
 
 
+class _PinnedPool:
+    """Pinned host receive buffers, recycled once the GPU copied out of them.
+
+    Pinning is slow (and serialises with the device), so buffers are never
+    freed during a fetch, and each is allocated with 25% headroom so the next
+    chunks' slightly different payload sizes reuse it."""
+
+    def __init__(self):
+        self._free: list[torch.Tensor] = []
+        self._lock = threading.Lock()
+
+    def get(self, n: int) -> torch.Tensor:
+        with self._lock:
+            fits = [k for k, b in enumerate(self._free) if b.numel() >= n]
+            if fits:
+                k = min(fits, key=lambda k: self._free[k].numel())
+                return self._free.pop(k)[:n]
+        return torch.empty(max(n + n // 4, 1 << 20), dtype=torch.uint8, pin_memory=True)[:n]
+
+    def put(self, bufs, event) -> None:
+        event.synchronize()  # the H2D copies that read these buffers are done
+        with self._lock:
+            for b in bufs:
+                self._free.append(b._base if b._base is not None else b)
+
+    def warm(self, n: int, count: int) -> None:
+        """Make sure `count` free buffers hold payloads of about n bytes."""
+        with self._lock:
+            have = sum(1 for b in self._free if b.numel() >= n)
+        bufs = [self.get(n) for _ in range(max(0, count - have))]
+        with self._lock:
+            self._free.extend(b._base if b._base is not None else b for b in bufs)
+
+
+_RECEIVE_POOL = _PinnedPool()   # shared by every fetch of the process: pin once
+
+
+def _mem_for(mem, cache_id):
+    return mem.get(cache_id, mem.get(cache_id.hex())) if isinstance(mem, dict) else mem
+
+
 def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=None,
                         initial_active="R1080", timeout_s=30.0, on_chunk=None, *, mem=None,
-                        scales_dtype_out=None, real_layers=None, depth=2):
+                        scales_dtype_out=None, real_layers=None, depth=32, max_batch=32,
+                        fetch_fn=None, workers=2):
     """Fetch chunks from a live server and decode them on the GPU as they arrive.
 
     ``chunks``: list of (cache_id, chunk_index).  Without ``mem`` each chunk is
     decoded to its int8 slab and on_chunk(record, QuantizedKV) is called, like
-    the reference.  With a PagedMemory ``mem`` each chunk is restored straight
-    into it (token_base = token_start, layer_base = 3 * layer_triplet_index,
-    dequantised with the container scales unless the cache holds int8) and
-    on_chunk(record, stats) receives the tokens written.  Up to ``depth``
-    received chunks wait for the GPU worker.
+    the reference (fk/netstore.py:367-454).  With ``mem`` — a PagedMemory, or a
+    dict cache_id -> PagedMemory (e.g. one for K, one for V) — each chunk is
+    restored straight into it (token_base = token_start, layer_base =
+    3 * layer_triplet_index, dequantised with the container scales unless the
+    cache holds int8) and on_chunk(record, stats) receives the tokens written.
+
+    Receive and GPU work overlap: payloads land in pinned host buffers;
+    ``workers`` GPU worker threads, each with its own CUDA stream, take every
+    chunk received so far (up to ``max_batch``; at most ``depth`` wait) and
+    decode them in ONE codec.decode_batch (a stream's decode is serial, so
+    batching chunks — and running batches concurrently — is what fills the
+    GPU), then restore them with one batched restore launch.  Chunks write
+    disjoint slots, so concurrent batches need no ordering; the host-side slot
+    claims are serialised by a lock.
+
+    ``fetch_fn`` replaces the network round trip (default netstore.fetch_chunk,
+    same signature); it is how a modelled link is replayed against the real
+    GPU pipeline.
     """
+    fetch_fn = fetch_fn or NS.fetch_chunk
     fixed = _fixed_policy(policy)
     timeline = FetchTimeline(policy=policy)
     base = time.monotonic()
     work = queue.Queue(maxsize=max(1, depth))
     errors = []
-    gpu_stream = torch.cuda.Stream()
     state = {"dec_end": None}
+    pool = _RECEIVE_POOL
+    claim_lock = threading.Lock()   # PagedMemory host state + timeline bookkeeping
+
+    def run_batch(items, gpu_stream):
+        t0 = time.monotonic()
+        held = 0
+        with torch.cuda.stream(gpu_stream):
+            if mem is None:
+                results = [NS.decode_fetched(meta, payload) for _, meta, payload in items]
+            else:
+                conts = [NS.container_of(meta, b"") for _, meta, _ in items]
+                frames, held = codec.decode_batch([p for _, _, p in items], stream=gpu_stream)
+                units = []
+                with claim_lock:  # claim every unit, then describe (pools may grow)
+                    for cont, fr, (_, meta, _) in zip(conts, frames, items):
+                        code = L.RESOLUTION_CODE[meta["resolution"]]
+                        m = _mem_for(mem, cont.cache_id)
+                        sc = None if m.dtype == torch.int8 else cont.scales()
+                        units.append(restore_unit(fr, cont.plan(code), m,
+                                                  3 * cont.layer_triplet_index,
+                                                  cont.token_start, sc, real_layers))
+                    restore_units(units, stream=gpu_stream)
+                results = [{"tokens_written": u.tokens_written} for u in units]
+            done = torch.cuda.Event()
+            done.record(gpu_stream)
+        pool.put([p for _, _, p in items if isinstance(p, torch.Tensor)], done)
+        gpu_stream.synchronize()
+        t1 = time.monotonic()
+        with claim_lock:
+            for rec, _, _ in items:
+                rec.update(decode_start=t0 - base, decode_end=t1 - base, tau_dec=t1 - t0,
+                           batch=len(items))
+            if state["dec_end"] is not None:
+                bubble = max(0.0, t0 - base - state["dec_end"])
+                items[0][0]["bubble"] = bubble
+                timeline.total_bubble += bubble
+            state["dec_end"] = max(t1 - base, state["dec_end"] or 0.0)
+            timeline.peak_restore_bytes = max(timeline.peak_restore_bytes, held)
+        if on_chunk is not None:
+            for (rec, _, _), res in zip(items, results):
+                on_chunk(rec, res)
 
     def gpu_worker():
+        gpu_stream = torch.cuda.Stream()
         while True:
             item = work.get()
             if item is None:
+                work.put(None)  # let the other workers see the end too
                 return
-            rec, meta, payload = item
+            items, stop = [item], False
+            while len(items) < max_batch:
+                try:
+                    nxt = work.get_nowait()
+                except queue.Empty:
+                    break
+                if nxt is None:
+                    stop = True
+                    work.put(None)
+                    break
+                items.append(nxt)
             try:
-                t0 = time.monotonic()
-                with torch.cuda.stream(gpu_stream):
-                    if mem is None:
-                        result = NS.decode_fetched(meta, payload)
-                        held = 0
-                    else:
-                        cont = NS.container_of(meta, payload)
-                        code = L.RESOLUTION_CODE[meta["resolution"]]
-                        plan = cont.plan(code)
-                        frames, held = codec.decode_batch([payload], stream=gpu_stream)
-                        sc = None if mem.dtype == torch.int8 else torch.from_numpy(cont.scales())
-                        n = restore_frames(frames[0], plan, mem, 3 * cont.layer_triplet_index,
-                                           cont.token_start, scales=sc, real_layers=real_layers,
-                                           stream=gpu_stream)
-                        result = {"tokens_written": n}
-                gpu_stream.synchronize()
-                t1 = time.monotonic()
-                rec.update(decode_start=t0 - base, decode_end=t1 - base, tau_dec=t1 - t0)
-                if state["dec_end"] is not None:
-                    rec["bubble"] = max(0.0, t0 - base - state["dec_end"])
-                    timeline.total_bubble += rec["bubble"]
-                state["dec_end"] = t1 - base
-                timeline.peak_restore_bytes = max(timeline.peak_restore_bytes, held)
-                if on_chunk is not None:
-                    on_chunk(rec, result)
+                if not errors:
+                    run_batch(items, gpu_stream)
             except Exception as e:  # surfaced on the caller's thread
                 errors.append(e)
+            if stop:
+                return
 
-    worker = threading.Thread(target=gpu_worker, daemon=True)
-    worker.start()
+    pool_threads = [threading.Thread(target=gpu_worker, daemon=True)
+                    for _ in range(max(1, workers))]
+    for t in pool_threads:
+        t.start()
     history, active = [], initial_active
     try:
         for i, (cache_id, chunk_index) in enumerate(chunks):
@@ -197,9 +286,13 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 res = select_resolution(bw, 1, active, table)
             active = res
             t_start = time.monotonic()
-            payload, meta, tau = NS.fetch_chunk(address, cache_id, chunk_index, res, timeout_s)
+            payload, meta, tau = fetch_fn(address, cache_id, chunk_index, res, timeout_s,
+                                          alloc=pool.get if mem is not None else None)
+            if i == 0 and mem is not None:  # in flight at most: the queue + the batches
+                pool.warm(payload.numel(), depth + workers)
             t_end = time.monotonic()
-            history.append((len(payload), tau))
+            history.append((payload.numel() if isinstance(payload, torch.Tensor) else len(payload),
+                            tau))
             rec = {"chunk": i, "resolution": res, "bw_est_gbps": bw,
                    "transfer_start": t_start - base, "transfer_end": t_end - base,
                    "tau_trans": tau, "decode_start": None, "decode_end": None, "tau_dec": None,
@@ -208,7 +301,8 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
             work.put((rec, meta, payload))
     finally:
         work.put(None)
-        worker.join()
+        for t in pool_threads:
+            t.join()
     if errors:
         raise errors[0]
     timeline.ttft = state["dec_end"] if state["dec_end"] is not None else 0.0

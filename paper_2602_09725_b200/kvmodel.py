@@ -171,6 +171,7 @@ class PagedMemory:
         self._free: list[int] = []
         self._cap_blocks = 0
         self._table = None                     # device int32 [cap_pages]
+        self._upload_stream = None
         self._table_host = np.zeros(0, np.int32)
         self._table_dirty = False
         self._written = np.zeros((0, 0), bool)   # [token, layer] write-once markers
@@ -196,6 +197,10 @@ class PagedMemory:
         if n <= self._cap_blocks:
             return
         new_cap = max(n, 2 * self._cap_blocks, 16)
+        if self._cap_blocks and self.layers:
+            # restores already launched (any stream) may still write the old
+            # pool: let them land before it is copied and released
+            torch.cuda.synchronize()
         for k, t in enumerate(self.layers):
             grown = torch.empty((new_cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             grown[: t.shape[0]].copy_(t)
@@ -216,9 +221,19 @@ class PagedMemory:
             setattr(self, name, new)
 
     def block_table(self) -> torch.Tensor:
-        """Device int32 table logical page -> physical block (-1 = unmapped)."""
+        """Device int32 table logical page -> physical block (-1 = unmapped).
+
+        A changed table is uploaded as a new tensor on an idle side stream (a
+        pageable copy would otherwise wait for all work queued on the caller's
+        stream) and the caller's stream waits for that upload only."""
         if self._table is None or self._table_dirty:
-            self._table = torch.from_numpy(self._table_host.copy()).to(_dev.device())
+            if self._upload_stream is None:
+                self._upload_stream = torch.cuda.Stream()
+            host = torch.from_numpy(self._table_host.copy()).pin_memory()
+            with torch.cuda.stream(self._upload_stream):
+                self._table = host.to(_dev.device(), non_blocking=True)
+            self._table.record_stream(torch.cuda.current_stream())
+            torch.cuda.current_stream().wait_stream(self._upload_stream)
             self._table_dirty = False
         return self._table
 

@@ -23,6 +23,66 @@ def _pad_mask(mem: PagedMemory, layer_base: int, real_layers: int | None):
     return tuple(layer_base + p >= real_layers for p in range(3))
 
 
+class RestoreUnit:
+    """One chunk's restore: slots claimed in the PagedMemory (write-once check,
+    page mapping, byte accounting — host side, as the reference's page_write,
+    fk/kvmodel.py:216-229), then a kvf_restore_unit descriptor built by
+    ``describe()``.  Claim every unit of a batch before describing any: a claim
+    may grow the cache's block pool, which moves its storage."""
+
+    def __init__(self, frames, plan, mem, layer_base, token_base, scales, real_layers,
+                 first_frame, n_frames):
+        n_frames = plan.frame_count - first_frame if n_frames is None else n_frames
+        if frames.shape[0] == plan.frame_count:
+            base_frame = 0
+        elif frames.shape[0] == n_frames:
+            base_frame = first_frame
+        else:
+            raise ValueError("frames must hold the restored range or the whole chunk")
+        cfg = plan.cfg
+        self.pad = _pad_mask(mem, layer_base, real_layers)
+        toks = np.asarray(plan.tokens_in_frames(first_frame, n_frames), np.int64) + token_base
+        mem._claim(toks, [layer_base + p for p in range(3) if not self.pad[p]], cfg.H, cfg.D)
+        self.scales = None
+        if mem.dtype != torch.int8:
+            if scales is None:
+                raise ValueError("a dequantising restore needs the chunk scales")
+            self.scales = _dev.to_device(scales, torch.float32).contiguous()
+            self.group_size = (cfg.H * cfg.D) // self.scales.shape[1]
+        else:
+            self.group_size = (cfg.H * cfg.D if scales is None
+                               else (cfg.H * cfg.D) // np.shape(scales)[1])
+        self.frames, self.plan, self.mem = frames, plan, mem
+        self.layer_base, self.token_base = layer_base, token_base
+        self.first_frame, self.n_frames, self.base_frame = first_frame, max(n_frames, 0), base_frame
+        self.tokens_written = len(toks)
+        self.desc = None
+
+    def describe(self) -> _lib.kvf_restore_unit:
+        u = _lib.kvf_restore_unit()
+        u.frames = _dev.surface_of(self.frames)
+        # Shift the surface so frame index first_frame maps onto frames[0].
+        u.frames.base = u.frames.base - self.base_frame * u.frames.frame_stride
+        u.plan = self.plan.to_c(self.group_size)
+        u.scales = None if self.scales is None else self.scales.data_ptr()
+        u.dst = self.mem.paged_view(self.layer_base, self.token_base, self.pad)
+        self._table = self.mem.block_table()   # the descriptor points into it
+        u.first_frame = self.first_frame
+        u.n_frames = self.n_frames
+        self.desc = u
+        return u
+
+
+def restore_unit(frames: torch.Tensor, plan: FramePlan, mem: PagedMemory, layer_base: int = 0,
+                 token_base: int = 0, scales=None, real_layers: int | None = None,
+                 first_frame: int = 0, n_frames: int | None = None) -> RestoreUnit:
+    """Claim the slots of frames [first_frame, first_frame + n_frames) of one
+    chunk (``frames`` holds exactly those frames or the whole chunk); describe
+    it later with RestoreUnit.describe() / restore_units."""
+    return RestoreUnit(frames, plan, mem, layer_base, token_base, scales, real_layers,
+                       first_frame, n_frames)
+
+
 def restore_frames(frames: torch.Tensor, plan: FramePlan, mem: PagedMemory,
                    layer_base: int = 0, token_base: int = 0, scales=None,
                    first_frame: int = 0, n_frames: int | None = None,
@@ -38,31 +98,10 @@ def restore_frames(frames: torch.Tensor, plan: FramePlan, mem: PagedMemory,
     n_frames = plan.frame_count - first_frame if n_frames is None else n_frames
     if n_frames <= 0:
         return 0
-    if frames.shape[0] == plan.frame_count:
-        base_frame = 0
-    elif frames.shape[0] == n_frames:
-        base_frame = first_frame
-    else:
-        raise ValueError("frames must hold the restored range or the whole chunk")
-    cfg = plan.cfg
-    pad = _pad_mask(mem, layer_base, real_layers)
-    toks = np.asarray(plan.tokens_in_frames(first_frame, n_frames), np.int64) + token_base
-    mem._claim(toks, [layer_base + p for p in range(3) if not pad[p]], cfg.H, cfg.D)
-    G_scales = None
-    if mem.dtype != torch.int8:
-        if scales is None:
-            raise ValueError("a dequantising restore needs the chunk scales")
-        G_scales = _dev.to_device(scales, torch.float32).contiguous()
-        group_size = (cfg.H * cfg.D) // G_scales.shape[1]
-    else:
-        group_size = cfg.H * cfg.D if scales is None else (cfg.H * cfg.D) // np.shape(scales)[1]
-    surf = _dev.surface_of(frames)
-    # Shift the surface so frame index first_frame maps onto frames[0].
-    surf.base = surf.base - base_frame * surf.frame_stride
-    dst = mem.paged_view(layer_base, token_base, pad)
-    _lib.call("kvf_restore", surf, first_frame, n_frames, plan.to_c(group_size),
-              _dev.ptr(G_scales), dst, _dev.stream_ptr(stream))
-    return len(toks)
+    ru = restore_unit(frames, plan, mem, layer_base, token_base, scales, real_layers,
+                      first_frame, n_frames)
+    restore_units([ru], stream)
+    return ru.tokens_written
 
 
 def _chain_batches(ix, batch_frames):
@@ -114,9 +153,13 @@ def restore_chunk_wise(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_
 
 
 def restore_units(units, stream=None) -> None:
-    """Batched restore of prepared kvf_restore_unit descriptors (one call, few launches)."""
-    arr = (_lib.kvf_restore_unit * len(units))(*units)
-    _lib.call("kvf_restore_batch", arr, len(units), _dev.stream_ptr(stream))
+    """Batched restore of prepared units (RestoreUnit or raw kvf_restore_unit
+    descriptors) in one libkvf call — one launch per 128 units."""
+    descs = [u.describe() if isinstance(u, RestoreUnit) else u for u in units]
+    if not descs:
+        return
+    arr = (_lib.kvf_restore_unit * len(descs))(*descs)
+    _lib.call("kvf_restore_batch", arr, len(descs), _dev.stream_ptr(stream))
 
 
 def make_restore_unit(frames: torch.Tensor, plan: FramePlan, scales: torch.Tensor | None,

@@ -1,0 +1,199 @@
+"""C5: pipelined chunked fetch of a Llama-3-8B 32K K+V context over a rate-limited
+loopback link (BASELINE.json configs[4]), GPU decode + restore into paged bf16.
+
+    python tools/bench_fetch_live.py [--rates 10,25,100,0] [--res R240,R1080]
+
+Packs the context into the reference's containers (88 units: K/V x 11 layer
+triplets x 4 chunks of <= 10,000 tokens; scales over all tokens, as
+fk/cli.py:222-224), writes them to a ChunkStore directory, serves it with the
+reference wire protocol and a token-bucket egress limit (fk/netstore.py:188-211),
+and runs live_fetch_pipeline into two PagedMemory caches (K and V).  Prints one
+JSON line per (resolution, rate): time to ready (first request -> last restore
+complete), the link time the coded bytes need at that rate, the rate the
+loopback actually delivered, batching, and a sampled bit-exactness check of
+the restored bf16 cache against dequantised codes.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import shutil
+import sys
+import tempfile
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2602_09725_b200 import container as C, fetch as FE, kvmodel as KV  # noqa: E402
+from paper_2602_09725_b200 import layout as L, netstore as NS  # noqa: E402
+
+
+def build_store(root, T, Lyr, H, D, resolutions, chunk=10_000):
+    cfg = L.identity_layout(H, D)
+    chunks, qs = [], {}
+    for kv_i, name in enumerate(("K", "V")):
+        cid = bytes([0x40 + kv_i]) * 16
+        x = KV.gen_synthetic_kv(T, Lyr, H, D, 0.9, kv_i, 0.3, dtype=torch.bfloat16)
+        q = KV.quantize(x.pad_layers())
+        qs[cid] = q
+        for j in range((Lyr + 2) // 3):
+            for c, t0 in enumerate(range(0, T, chunk)):
+                tc = min(chunk, T - t0)
+                slab = KV.QuantizedKV(q.values[t0:t0 + tc, 3 * j:3 * j + 3],
+                                      q.scales[3 * j:3 * j + 3], q.group_size)
+                idx = j * 1000 + c
+                cont = C.pack_chunk(slab, cfg, resolutions, cache_id=cid, chunk_index=idx,
+                                    token_start=t0, layer_triplet_index=j)
+                with open(os.path.join(root, C.container_filename(cid, idx)), "wb") as fh:
+                    fh.write(cont.to_bytes())
+                chunks.append((cid, idx))
+        del x
+    return chunks, qs
+
+
+def serve_proc(root, rate, port_q, stop):
+    handle = NS.serve(NS.ChunkStore(root, preload=True), ("127.0.0.1", 0), rate_limit_gbps=rate)
+    port_q.put(handle.address[1])
+    stop.wait()
+    handle.close()
+
+
+class ModelLink:
+    """A modelled link replayed against the real pipeline: chunk i is handed
+    over (from pinned memory) when its last byte would have arrived at `rate`
+    Gbps after the first request, i.e. a constant-rate BandwidthTrace
+    (fk/fetchsim.py:93-139).  Isolates the GPU side from Python socket speed."""
+
+    def __init__(self, store, rate_gbps):
+        self.store, self.rate = store, rate_gbps * 1e9
+        self.t0, self.sent, self.pinned = None, 0, {}
+
+    def stage(self, chunks, code):
+        for cid, idx in chunks:
+            meta, payload = self.store.lookup(cid, idx, code)
+            t = torch.frombuffer(bytearray(payload), dtype=torch.uint8).pin_memory()
+            self.pinned[(cid, idx)] = (meta, t)
+
+    def __call__(self, address, cache_id, chunk_index, resolution, timeout_s=30.0, alloc=None):
+        now = time.monotonic()
+        if self.t0 is None:
+            self.t0 = now
+        meta, t = self.pinned[(bytes(cache_id), chunk_index)]
+        self.sent += t.numel()
+        arrive = self.t0 + self.sent * 8 / self.rate
+        if arrive > now:
+            time.sleep(arrive - now)
+        return t, meta, time.monotonic() - now
+
+
+def new_mems(qs, T, Lyr, H, D):
+    """One paged bf16 pool per cache (K, V), preallocated like a serving engine's
+    KV pool: ceil(T / 16) blocks x the padded layers."""
+    return {cid: KV.PagedMemory(16, dtype=torch.bfloat16, H=H, D=D, num_blocks=-(-T // 16),
+                                num_layers=3 * ((Lyr + 2) // 3)) for cid in qs}
+
+
+def check(mems, qs, Lyr, T, n=64):
+    g = torch.Generator().manual_seed(0)
+    bad = 0
+    for cid, q in qs.items():
+        mem = mems[cid]
+        for _ in range(n):
+            t = int(torch.randint(0, T, (1,), generator=g))
+            l = int(torch.randint(0, Lyr, (1,), generator=g))
+            want = (q.values[t, l].float().reshape(q.H * q.D // q.group_size, -1)
+                    * q.scales[l].reshape(-1, 1)).reshape(-1).to(torch.bfloat16)
+            bad += int(not torch.equal(mem.read(t, l), want))
+    return bad
+
+
+def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
+    recs = tl.records
+    first = min(r["transfer_start"] for r in recs)
+    last_rx = max(r["transfer_end"] for r in recs)
+    line = {
+        "config": "C5: llama3-8b K+V 32K, 88 chunks, pipelined fetch -> GPU decode -> "
+                  "paged bf16 restore", "link": link, "resolution": res,
+        "rate_gbps": rate, "coded_bytes": coded,
+        "ready_s": round(tl.ttft - first, 4),
+        "link_s_at_rate": round(coded * 8 / (rate * 1e9), 4) if rate else None,
+        "receive_s": round(last_rx - first, 4),
+        "delivered_gbps": round(coded * 8 / (last_rx - first) / 1e9, 2),
+        "tail_after_last_byte_s": round(tl.ttft - last_rx, 4),
+        "decode_batches": len({r["decode_start"] for r in recs}),
+        "max_batch": max(r.get("batch", 1) for r in recs),
+        "total_bubble_s": round(tl.total_bubble, 4),
+        "sampled_slots_mismatch": check(mems, qs, Lyr, args.tokens),
+        "setup_pack_s": round(setup_s, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tokens", type=int, default=32768)
+    ap.add_argument("--rates", default="10,25,100,0", help="Gbps; 0 = unthrottled loopback")
+    ap.add_argument("--res", default="R240,R1080")
+    ap.add_argument("--dir", default=None)
+    ap.add_argument("--link", default="model", choices=["model", "tcp"],
+                    help="model: constant-rate arrival replay; tcp: live loopback server")
+    args = ap.parse_args()
+    Lyr, H, D = 32, 8, 128
+    resolutions = args.res.split(",")
+    root = args.dir or tempfile.mkdtemp(prefix="kvfc_store_")
+    t0 = time.perf_counter()
+    chunks, qs = build_store(root, args.tokens, Lyr, H, D, resolutions)
+    setup_s = time.perf_counter() - t0
+    store = NS.ChunkStore(root)
+    ctx = mp.get_context("spawn")
+    for res in resolutions:
+        code = L.RESOLUTION_CODE[res]
+        coded = sum(store.index[(cid, idx)]["entries"][code][1] for cid, idx in chunks)
+        # untimed warm-up: pins the receive pool, grows the allocator, loads kernels
+        link = ModelLink(store, 1000.0)
+        link.stage(chunks, code)
+        FE.live_fetch_pipeline(None, chunks, None, f"fixed:{res}",
+                               mem=new_mems(qs, args.tokens, Lyr, H, D), real_layers=Lyr,
+                               fetch_fn=link)
+        del link
+        for rate in [float(r) for r in args.rates.split(",")] if args.link == "model" else []:
+            link = ModelLink(store, rate)
+            link.stage(chunks, code)
+            mems = new_mems(qs, args.tokens, Lyr, H, D)
+            torch.cuda.synchronize()
+            tl = FE.live_fetch_pipeline(None, chunks, None, f"fixed:{res}", mem=mems,
+                                        real_layers=Lyr, fetch_fn=link)
+            emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, "modelled constant-rate link")
+            del mems, link
+            torch.cuda.empty_cache()
+        for rate in [float(r) for r in args.rates.split(",")] if args.link == "tcp" else []:
+            # the chunk server runs in its own process (a remote node's role):
+            # it does not share this process's GIL with the fetcher
+            port_q, stop = ctx.Queue(), ctx.Event()
+            srv = ctx.Process(target=serve_proc, args=(root, rate or None, port_q, stop))
+            srv.start()
+            mems = new_mems(qs, args.tokens, Lyr, H, D)
+            try:
+                addr = f"127.0.0.1:{port_q.get(timeout=120)}"
+                torch.cuda.synchronize()
+                tl = FE.live_fetch_pipeline(addr, chunks, None, f"fixed:{res}", mem=mems,
+                                            real_layers=Lyr)
+            finally:
+                stop.set()
+                srv.join(timeout=30)
+            emit(tl, res, rate or None, coded, mems, qs, Lyr, args, setup_s,
+                 "loopback TCP, reference wire protocol, token-bucket egress")
+            del mems
+            torch.cuda.empty_cache()
+    if args.dir is None:
+        shutil.rmtree(root, ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
