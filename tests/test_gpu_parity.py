@@ -338,3 +338,48 @@ def test_c2_unit_round_trip_property():
             for p in range(3)], dim=1)
         want = q.values if dt == torch.int8 else KV.dequantize(q, torch.bfloat16).data
         assert torch.equal(cache, want)
+
+
+@pytest.mark.parametrize("shape", [
+    # (name, H, D, layers, triplet, T, res, layout): a full 10,000-token unit of each
+    # BASELINE.json model, checked against the CPU oracle (quantize + assemble + slots)
+    ("qwen2.5-7b C3 (4 KV heads, 28 -> 30 layers)", 4, 128, 28, 9, 10000, "R640", "paper"),
+    ("llama3-70b C4 (80 -> 81 layers, pad layer)", 8, 128, 80, 26, 10000, "R1080", "identity"),
+    ("llama3-8b C2 last chunk", 8, 128, 32, 10, 2768, "R240", "identity"),
+])
+def test_baseline_config_units_match_oracle(shape):
+    name, H, D, Lyr, j, T, res, layout = shape
+    gs = 128
+    real = min(3, Lyr - 3 * j)
+    lay = (H, D, 1, H, 1, D) if layout == "identity" else (H, D, H, 1, 1, D)
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, real, H, D, 0.9, 5, 0.3))
+    xp = np.concatenate([x, np.zeros((T, 3 - real, H, D), np.float32)], axis=1)
+    v, s = ref.quantize(xp, gs)                              # oracle: pad layer -> scale 1
+    oplan = ref.Plan(T, res, *lay, F=4)
+    want_frames = ref.assemble_frames(v.reshape(T, 3, H * D), oplan)
+    # GPU: pack from the [T, real, H, D] bf16 cache (pad layer = NULL pointer)
+    kv = np_bf16_from_f32(x).cuda()
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+    fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
+    am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)), dtype=torch.int32,
+                     device="cuda")
+    sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
+    u, _ = _pack_unit(kv, lay, res, 0, T, 4, gs, fr, am, sc)
+    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(sc.cpu().numpy(), s, err_msg=name)
+    np.testing.assert_array_equal(fr.cpu().numpy(), want_frames, err_msg=name)
+    # restore the oracle's frames into a paged bf16 cache (layers 3j.., pad layer unwritten)
+    mem = KV.PagedMemory(16, dtype=torch.bfloat16)
+    n = restore_frames(torch.from_numpy(want_frames).cuda(), plan, mem, layer_base=3 * j,
+                       token_base=0, scales=torch.from_numpy(s), real_layers=Lyr)
+    assert n == T
+    deq = torch.from_numpy(ref.dequantize(v, s, gs)).to(torch.bfloat16)
+    rng = np.random.default_rng(1)
+    for t in np.r_[0, T - 1, rng.integers(0, T, 64)]:
+        for p in range(3):
+            got = mem.read(int(t), 3 * j + p)
+            if p >= real:
+                assert got is None                               # pad layer never written
+            else:
+                assert torch.equal(got.cpu(), deq[t, p].reshape(-1)), (name, t, p)
