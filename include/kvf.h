@@ -133,7 +133,7 @@ typedef struct kvf_pack_unit {
   kvf_paged src;           /* bf16/f16/f32 KV to quantize, or int8 codes */
   kvf_plan plan;
   uint32_t* absmax;        /* device scratch of kvf_pack_scratch_words(&plan) u32:
-                              [3, G] |x| maxima (f32 bit patterns) + 4 control words */
+                              [3, G] |x| maxima (f32 bit patterns) + [3, G] counters */
   float* scales;           /* device [3, G] out (ignored for int8 sources) */
   kvf_surface frames;      /* out: frame_count frames */
 } kvf_pack_unit;
@@ -185,14 +185,12 @@ kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan,
                            const uint32_t* absmax, float* scales,
                            const kvf_surface* frames, void* stream);
 
-/* Both phases for up to n_units units, zeroing each unit's scratch first.
- * Quantising units on the fast path run as ONE persistent launch in which each
- * (unit, plane)'s quantise tiles wait on its absmax tiles through counters in
- * the scratch, so the second read of the source is served from L2. */
+/* Both phases for up to n_units units, zeroing each unit's scratch first:
+ * absmax -> scales -> frames, a handful of launches for any number of units. */
 kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
                           void* stream);
 
-/* u32 words of pack scratch a unit of this plan needs: 3*G + 4. */
+/* u32 words of pack scratch a unit of this plan needs: 6*G (G = H*D/group_size). */
 int64_t kvf_pack_scratch_words(const kvf_plan* plan);
 
 /* ---- whole-tensor quantize / dequantize (fk/kvmodel.py:127-152) -------- */

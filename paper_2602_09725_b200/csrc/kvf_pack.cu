@@ -1,17 +1,15 @@
-// kvf_pack.cu — (paged) KV -> quantised 3-plane frames, sm_100a: entry points,
-// the phase-split kernels and the L2-reuse fused fallback.
+// kvf_pack.cu — (paged) KV -> quantised 3-plane frames, sm_100a: entry points
+// and the phase-split kernels.
 //
 // Replaces quantize (fk/kvmodel.py:127-144) + slice_tokens (fk/layout.py:109-114)
 // + assemble_frames (fk/layout.py:234-258) for (layer triplet, token chunk) units.
 //
-// kvf_pack_batch picks, per group of units:
-//   1. pack_coop_kernel (kvf_pack_coop.cu): one cooperative launch, source
-//      staged once in SMEM by TMA bulk copies — 3 B of HBM traffic per element;
-//   2. pack_fused_kernel (below): persistent queue of absmax / quantise tiles
-//      with per-plane dependency counters; the second source read is served
-//      from L2 (evict_last on the first read) — for shapes that do not fit 1;
-//   3. the phase-split kernels (absmax -> scales -> frames), also used by the
-//      single-phase entry points and for int8 sources (assemble_frames).
+// kvf_pack_batch runs, per group of units sharing (variant, dtype):
+//   zero scratch -> absmax (max |x| per (plane, group) over all chunk tokens) ->
+//   scales -> frames (exact quantise + tile + place, pad tiles 128).
+// The reference scale spans all chunk tokens, so the source is read twice;
+// KVF_PACK_MODE=team selects the single-HBM-read team kernel
+// (kvf_pack_team.cu), measured slower on B200.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -22,8 +20,6 @@
 
 namespace kvf {
 
-kvf_status launch_pack_coop(const std::vector<kvf_pack_unit>& units, int32_t dtype,
-                            cudaStream_t s, bool* launched);
 kvf_status launch_pack_team(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                             cudaStream_t s, bool* launched);
 
@@ -265,154 +261,6 @@ __global__ void __launch_bounds__(kThreads)
   *dst = (uint8_t)(q + 128);
 }
 
-// ------------------------------------------------- L2-reuse fused fallback
-//
-// Single queue of tiles ordered A(0) | A(1) | A(2) Q(0) | A(3) Q(1) | ... where
-// A(s) computes the |x| maxima of sub-unit s = (unit, plane) and Q(s) quantises
-// it.  CTAs take tiles from an atomic counter; a Q tile of s waits for the
-// counter of s to reach its A-tile count.  A tiles of s precede its Q tiles in
-// the queue and a CTA waits only between tiles, so every awaited tile is held
-// by a running CTA (no deadlock, no co-residency requirement).  First reads
-// carry evict_last, re-reads and frame stores evict_first, so Q(s) re-reads
-// its slab from L2.
-constexpr int kATokPerWarp = 16;
-constexpr int kATok = kWarps * kATokPerWarp;  // tokens per A tile
-constexpr int kQPerWarp = 4;
-constexpr int kQItems = kWarps * kQPerWarp;   // frame slots per Q tile
-constexpr int kMaxFusedUnits = 96;
-constexpr int kMaxSub = 3 * kMaxFusedUnits;
-constexpr int kLag = 2;  // Q(s) sits kLag segments after A(s)
-
-struct FusedParams {
-  int32_t n_units;
-  int32_t n_sub;
-  int32_t total_tiles;
-  uint32_t* queue;
-  PackUnitDev u[kMaxFusedUnits];
-  int32_t seg_begin[kMaxSub + kLag + 1];  // segment s = A(s) + Q(s - kLag)
-  uint16_t n_a[kMaxSub];
-};
-
-template <int SRC, int VPL>
-__device__ __forceinline__ void fused_a_tile(const PackUnitDev& U, int p, int tile,
-                                             uint32_t* s_max) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
-  constexpr int ES = SRC == KVF_F32 ? 4 : 2;
-  for (int k = threadIdx.x; k < U.G; k += kThreads) s_max[k] = 0u;
-  __syncthreads();
-  int32_t off[VPL];
-  uint32_t m[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    off[k] = (int32_t)slot_channel_offset(U.g, (lane + 32 * k) * 8, U.src.head_stride) * ES;
-    m[k] = 0u;
-  }
-  const int tok0 = tile * kATok + warp * kATokPerWarp;
-  const WithPolicy keep{l2_policy_evict_last()};
-#pragma unroll 4
-  for (int t = 0; t < kATokPerWarp; ++t) {
-    int i = tok0 + t;
-    if (i >= U.g.T) break;
-    const char* slot = layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES;
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) m[k] = max(m[k], vec_absmax_bits<SRC>(slot + off[k], keep));
-  }
-  reduce_groups<SRC, VPL>(m, U.g.group_size, s_max);
-  __syncthreads();
-  for (int k = threadIdx.x; k < U.G; k += kThreads) {
-    if (s_max[k]) atomicMax(&U.absmax[p * U.G + k], s_max[k]);
-    __threadfence();  // each writer makes its reduction visible before the barrier
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(&U.done[p], 1u);
-}
-
-template <int SRC, int VPL>
-__device__ __forceinline__ void fused_q_tile(const PackUnitDev& U, int p, int tile, int n_a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0 && n_a > 0) {
-    long long spins = 0;
-    while (ld_acquire_u32(&U.done[p]) < (uint32_t)n_a) {
-      __nanosleep(128);
-      if (++spins == (1ll << 28)) __trap();  // broken schedule: fail hard, never hang
-    }
-  }
-  __syncthreads();
-  const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
-  constexpr int ES = SRC == KVF_F32 ? 4 : 2;
-  if (tile == 0)  // one CTA per sub-unit publishes the scales (fk/kvmodel.py:140)
-    for (int k = threadIdx.x; k < U.G; k += kThreads)
-      U.scales[p * U.G + k] = scale_from_absmax_bits(__ldcg(&U.absmax[p * U.G + k]));
-  int32_t in_off[VPL], tile_off[VPL];
-  float s[VPL], inv[VPL];
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    int c = (lane + 32 * k) * 8;
-    in_off[k] = (int32_t)slot_channel_offset(U.g, c, U.src.head_stride) * ES;
-    tile_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
-    s[k] = scale_from_absmax_bits(__ldcg(&U.absmax[p * U.G + (c >> U.g.lg_gs)]));
-    inv[k] = __frcp_rn(s[k]);
-  }
-  uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
-  const int q0 = tile * kQItems + warp * kQPerWarp;
-  const uint64_t drop = l2_policy_evict_first();
-  const WithPolicy last_use{drop};
-#pragma unroll 1
-  for (int it = 0; it < kQPerWarp; ++it) {
-    const int q = q0 + it;
-    if (q >= U.n_items) break;
-    const int f = fdiv(U.g.div_tpf, q);
-    const int slot = q - f * U.g.tpf;
-    const int i = token_of(U.g, f, slot);
-    const int tr = fdiv(U.g.div_cols, slot);
-    const int tc = slot - tr * U.g.grid_cols;
-    uint8_t* dst = plane_base + (int64_t)f * U.fr.frame_stride +
-                   (int64_t)tr * U.g.tile_h * U.fr.row_pitch + tc * U.g.tile_w;
-    if (i >= U.g.T || layer == nullptr) {
-#pragma unroll
-      for (int k = 0; k < VPL; ++k)
-        st_v2_pol(dst + tile_off[k], make_uint2(0x80808080u, 0x80808080u), drop);
-      continue;
-    }
-    const char* slotp = layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES;
-    constexpr int KB = VPL < 4 ? VPL : 4;
-#pragma unroll
-    for (int k0 = 0; k0 < VPL; k0 += KB) {
-      float x[KB][8];
-#pragma unroll
-      for (int k = 0; k < KB; ++k) load_vec8<SRC>(slotp + in_off[k0 + k], x[k], last_use);
-#pragma unroll
-      for (int k = 0; k < KB; ++k)
-        st_v2_pol(dst + tile_off[k0 + k], quantize8<false>(x[k], s[k0 + k], inv[k0 + k]), drop);
-    }
-  }
-}
-
-template <int SRC, int VPL>
-__global__ void __launch_bounds__(kThreads, 3)
-    pack_fused_kernel(const __grid_constant__ FusedParams P) {
-  extern __shared__ uint32_t s_max[];
-  __shared__ int s_tile;
-  int seg = 0;  // cursor into seg_begin (tiles arrive in increasing order per CTA)
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(P.queue, 1u);
-    __syncthreads();
-    const int t = s_tile;
-    if (t >= P.total_tiles) break;
-    while (P.seg_begin[seg + 1] <= t) ++seg;
-    const int local = t - P.seg_begin[seg];
-    const int na = seg < P.n_sub ? (int)P.n_a[seg] : 0;
-    if (local < na) {
-      fused_a_tile<SRC, VPL>(P.u[seg / 3], seg % 3, local, s_max);
-    } else {
-      const int s = seg - kLag;
-      fused_q_tile<SRC, VPL>(P.u[s / 3], s % 3, local - na, (int)P.n_a[s]);
-    }
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------- host
 bool aligned(const void* p, int64_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
@@ -556,91 +404,6 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32
   return KVF_OK;
 }
 
-template <int SRC, int VPL>
-kvf_status launch_fused_t(const FusedParams& P, size_t smem, cudaStream_t s) {
-  int dev = 0, sms = 0, occ = 0;
-  KVF_CHECK_CUDA(cudaGetDevice(&dev));
-  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  KVF_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &occ, pack_fused_kernel<SRC, VPL>, kThreads, smem));
-  int grid = std::max(1, std::min(P.total_tiles, sms * std::max(occ, 1)));
-  pack_fused_kernel<SRC, VPL><<<grid, kThreads, smem, s>>>(P);
-  KVF_CHECK_CUDA(cudaGetLastError());
-  return KVF_OK;
-}
-
-template <int SRC>
-kvf_status launch_fused_vpl(int vpl, const FusedParams& P, size_t smem, cudaStream_t s) {
-  switch (vpl) {
-    case 1: return launch_fused_t<SRC, 1>(P, smem, s);
-    case 2: return launch_fused_t<SRC, 2>(P, smem, s);
-    case 4: return launch_fused_t<SRC, 4>(P, smem, s);
-    case 8: return launch_fused_t<SRC, 8>(P, smem, s);
-    default: return launch_fused_t<SRC, 16>(P, smem, s);
-  }
-}
-
-kvf_status launch_fused_l2(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                           cudaStream_t s) {
-  FusedParams* P = new FusedParams();
-  P->n_units = (int32_t)units.size();
-  P->n_sub = (int32_t)(3 * units.size());
-  int max_G = 1;
-  for (size_t k = 0; k < units.size(); ++k) {
-    P->u[k] = make_pack_unit_dev(units[k]);
-    max_G = std::max(max_G, P->u[k].G);
-  }
-  P->queue = P->u[0].done + 3;
-  int32_t acc = 0;
-  const int n_seg = P->n_sub + kLag;
-  for (int sidx = 0; sidx < n_seg; ++sidx) {
-    P->seg_begin[sidx] = acc;
-    int na = 0;
-    if (sidx < P->n_sub) {
-      const PackUnitDev& U = P->u[sidx / 3];
-      na = U.src.layer[sidx % 3] ? (U.g.T + kATok - 1) / kATok : 0;
-      P->n_a[sidx] = (uint16_t)na;
-    }
-    int nq = 0;
-    const int sq = sidx - kLag;
-    if (sq >= 0) nq = (P->u[sq / 3].n_items + kQItems - 1) / kQItems;
-    acc += na + nq;
-  }
-  P->seg_begin[n_seg] = acc;
-  P->total_tiles = acc;
-  size_t smem = (size_t)max_G * sizeof(uint32_t);
-  kvf_status st;
-  switch (dtype) {
-    case KVF_BF16: st = launch_fused_vpl<KVF_BF16>(vpl, *P, smem, s); break;
-    case KVF_F16: st = launch_fused_vpl<KVF_F16>(vpl, *P, smem, s); break;
-    default: st = launch_fused_vpl<KVF_F32>(vpl, *P, smem, s); break;
-  }
-  delete P;
-  return st;
-}
-
-// Both phases for fast-variant quantising units: zero the scratch, then the
-// cooperative TMA kernel, else the L2-reuse fused kernel.
-kvf_status launch_fused_group(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                              cudaStream_t s) {
-  constexpr size_t kChunk = 64;  // units per fused launch
-  for (size_t at = 0; at < units.size(); at += kChunk) {
-    size_t n = std::min(kChunk, units.size() - at);
-    std::vector<kvf_pack_unit> part(units.begin() + at, units.begin() + at + n);
-    kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero scratch + counters
-    if (st != KVF_OK) return st;
-    bool launched = false;
-    const char* mode = getenv("KVF_PACK_MODE");
-    if (!(mode && strcmp(mode, "l2") == 0)) st = launch_pack_coop(part, dtype, s, &launched);
-    if (st != KVF_OK) return st;
-    if (!launched) {
-      st = launch_fused_l2(part, vpl, dtype, s);
-      if (st != KVF_OK) return st;
-    }
-  }
-  return KVF_OK;
-}
-
 // Zero the scratch, then the team kernel per launch-sized slice of units with
 // one group size; slices it cannot take run the phase-split kernels.
 kvf_status launch_team_group(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
@@ -683,23 +446,13 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, cudaStre
   for (int v = 0; v <= 16; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        // Default: the phase-split kernels (absmax pass, then quantise pass;
-        // fastest measured).  KVF_PACK_MODE=team selects the
-        // single-HBM-read team kernel (kvf_pack_team.cu), =fused|l2 the
-        // cooperative / L2-reuse schedules — all slower on B200.
+        // Default: the phase-split kernels (fastest measured);
+        // KVF_PACK_MODE=team selects the single-HBM-read team kernel.
         const char* mode = getenv("KVF_PACK_MODE");
-        const bool whole = v != 0 && dt != KVF_I8 && phases == (1 | 2 | 4 | 8);
-        const bool fused = whole && mode &&
-                           (strcmp(mode, "fused") == 0 || strcmp(mode, "l2") == 0);
-        const bool team = whole && mode && strcmp(mode, "team") == 0;
-        kvf_status st = KVF_OK;
-        if (fused) {
-          st = launch_fused_group(groups[v][dt], v, dt, s);
-        } else if (team) {
-          st = launch_team_group(groups[v][dt], v, dt, s);
-        } else {
-          st = launch_phases(groups[v][dt], v, dt, phases, s);
-        }
+        const bool team = v != 0 && dt != KVF_I8 && phases == (1 | 2 | 4 | 8) && mode &&
+                          strcmp(mode, "team") == 0;
+        kvf_status st = team ? launch_team_group(groups[v][dt], v, dt, s)
+                             : launch_phases(groups[v][dt], v, dt, phases, s);
         if (st != KVF_OK) return st;
       }
   return KVF_OK;

@@ -14,25 +14,18 @@ constexpr int kPackThreads = 256;
 constexpr int kPackWarps = kPackThreads / 32;
 constexpr int kMaxPackUnits = 96;  // descriptors per launch (kernel params <= 32 KB)
 
-// Scratch words of a unit (kvf_pack_scratch_words): [3, G] maxima | 3 per-plane
-// done counters | 1 queue word | 3 * (C/256) per-stripe counters | [3, G]
-// per-(plane, group) team counters.
-inline int64_t pack_stripe_words(const kvf_plan& p) {
-  const int64_t C = (int64_t)p.H * p.D;
-  return 3 * (C >= 256 ? C / 256 : 1);
-}
+// Scratch words of a unit (kvf_pack_scratch_words): [3, G] |x| maxima (f32
+// bit patterns) | [3, G] per-(plane, group) counters of the team kernel.
 inline int64_t pack_scratch_words(const kvf_plan& p) {
   const int64_t G = (int64_t)p.H * p.D / p.group_size;
-  return 3 * G + 4 + pack_stripe_words(p) + 3 * G;
+  return 6 * G;
 }
 
 struct PackUnitDev {
   kvf_paged src;
   Geom g;
   uint32_t* absmax;       // [3, G] maxima (f32 bit patterns)
-  uint32_t* done;         // absmax + 3G: per-plane counters, then the queue word
-  uint32_t* stripe_done;  // absmax + 3G + 4: per-(plane, stripe) counters
-  uint32_t* team_done;    // then [3, G] per-(plane, group) team counters
+  uint32_t* team_done;    // absmax + 3G: [3, G] per-(plane, group) team counters
   float* scales;
   kvf_surface fr;
   FastDiv div_bs;
@@ -47,9 +40,7 @@ inline PackUnitDev make_pack_unit_dev(const kvf_pack_unit& u) {
   d.g = make_geom(u.plan);
   d.G = (u.plan.H * u.plan.D) / u.plan.group_size;
   d.absmax = u.absmax;
-  d.done = u.absmax ? u.absmax + 3 * d.G : nullptr;
-  d.stripe_done = u.absmax ? u.absmax + 3 * d.G + 4 : nullptr;
-  d.team_done = u.absmax ? d.stripe_done + pack_stripe_words(u.plan) : nullptr;
+  d.team_done = u.absmax ? u.absmax + 3 * d.G : nullptr;
   d.n_scratch = (int32_t)pack_scratch_words(u.plan);
   d.scales = u.scales;
   d.fr = u.frames;
@@ -58,7 +49,7 @@ inline PackUnitDev make_pack_unit_dev(const kvf_pack_unit& u) {
   return d;
 }
 
-// Source vector loads; the fused kernel tags them with an L2 eviction policy.
+// Source vector loads; the team kernel tags its re-reads with an L2 eviction policy.
 struct NoPolicy {
   __device__ __forceinline__ uint4 load(const char* p) const { return ld_nc_v4(p); }
 };

@@ -1,4 +1,5 @@
-"""GPU stress: repeat the fused pack many times per config, count mismatches vs oracle."""
+"""GPU stress: repeat kvf_pack_batch (KVF_PACK_MODE selects the schedule) many times per config,
+count mismatches vs the oracle."""
 import os
 import sys
 import time
