@@ -4,11 +4,12 @@
 //    (fk/rangecoder.py:146-189), one thread per (frame, plane) stream — every
 //    stream resets its model and is length-prefixed, so they are independent.
 //    The per-symbol work is a serial dependency chain, so the kernel is built
-//    for latency: the top four Fenwick levels are registers, the second
-//    division is replaced by multiplies inside the descent, tree updates are
-//    fire-and-forget shared atomics, the halving rebuild is block-parallel,
-//    and payload words are prefetched one word ahead.  The root node (total)
-//    is never read by the search and is not stored.
+//    for latency and few instructions: the model is cumulative counts (block
+//    prefix sums in registers, within-block prefix sums as packed u16 in
+//    shared memory — 512 B per stream), both searches are 4-level binary
+//    searches over registers, the second division is replaced by multiplies,
+//    renormalisation is three predicated rounds over a prefetched 64-bit byte
+//    window, and a symbol's model update is two 128-bit stores.
 // 2. recon_kernel: per-sample prediction (fk/codec.py:131-144) as segmented
 //    prefix sums mod 256.  One CTA per chain of same-plane frames starting at
 //    an intra frame.  A 16-pixel run of a row never crosses a 16x16 block, so a
@@ -28,201 +29,277 @@ constexpr uint32_t kBot = 1u << 16;
 constexpr uint32_t kInc = 32;
 constexpr uint32_t kLimit = 1u << 16;
 
-// Sequential byte reader over a device payload; bytes past the end are 0.
-// Two aligned words are held: the one being consumed and the next one, whose
-// load is issued four bytes ahead so the dependent decode chain rarely waits.
-struct ByteStream {
-  uintptr_t wa;    // address of the aligned word `cur`
-  uintptr_t end;   // payload end address
-  uintptr_t a;     // address of the next byte
-  uint32_t cur, nxt;
+// Payload bytes through a 64-bit window: `win` holds the 8 bytes at [wa, wa+8),
+// the next byte is at `a` with a - wa < 4 at every symbol start.  A refill
+// shifts in the word prefetched one refill earlier (`nxt`), so the load never
+// sits on the decode chain.  Loads use clamped in-bounds addresses and bytes
+// at or past the end read as 0 (fk/rangecoder.py:158,181: data[pos] if pos < n).
+struct ByteWindow {
+  uint64_t win;
+  uintptr_t wa, a, end, last;  // last = the last aligned word holding payload bytes
+  uint32_t nxt;                // raw word at wa + 8 (loaded one refill ahead)
+  bool nxt_ok;                 // wa + 8 < end: otherwise it reads as 0
+  __device__ __forceinline__ uint32_t load(uintptr_t w) const {  // in bounds, unmasked
+    return __ldg(reinterpret_cast<const uint32_t*>(w < end ? w : last));
+  }
   __device__ __forceinline__ void init(const uint8_t* p, uint32_t n) {
     a = reinterpret_cast<uintptr_t>(p);
     end = a + n;
     wa = a & ~uintptr_t(3);
-    cur = n ? __ldg(reinterpret_cast<const uint32_t*>(wa)) : 0u;
-    nxt = wa + 4 < end ? __ldg(reinterpret_cast<const uint32_t*>(wa + 4)) : 0u;
-  }
-  // Straight-line (predicated) so the per-symbol renormalisation does not
-  // branch: the byte, then the word rotation when `a` crosses into `nxt`.
-  __device__ __forceinline__ uint32_t next() {
-    const uint32_t b = a < end ? (cur >> (8 * (a & 3))) & 0xFFu : 0u;
-    ++a;
-    if ((a & 3) == 0) {
-      wa += 4;
-      cur = nxt;
-      nxt = wa + 4 < end ? __ldg(reinterpret_cast<const uint32_t*>(wa + 4)) : 0u;
+    last = n ? (end - 1) & ~uintptr_t(3) : wa;
+    if (n == 0) {  // every byte reads as 0; never dereference
+      win = 0;
+      nxt = 0;
+      nxt_ok = false;
+      end = 0;
+      return;
     }
-    return b;
+    const uint32_t w0 = load(wa), w1 = wa + 4 < end ? load(wa + 4) : 0u;
+    win = (uint64_t)w0 | ((uint64_t)w1 << 32);
+    nxt = load(wa + 8);
+    nxt_ok = wa + 8 < end;
+  }
+  __device__ __forceinline__ uint32_t peek() const {  // byte at a (a - wa < 8)
+    return a < end ? (uint32_t)(win >> (8 * (a - wa))) & 0xFFu : 0u;
+  }
+  // The next n <= 3 bytes as a big-endian number (first byte most significant;
+  // bytes at or past the end are 0); advances a.  Needs a - wa < 4.
+  __device__ __forceinline__ uint32_t take(uint32_t n) {
+    uint32_t w = (uint32_t)(win >> (8 * (a - wa)));           // bytes a.. a+3, little-endian
+    const uintptr_t valid = end > a ? end - a : 0;            // bytes before the end
+    w = valid >= 4 ? w : w & ((1u << (8 * (uint32_t)valid)) - 1u);
+    const uint32_t be = __byte_perm(w, 0u, 0x0123);           // byte a in bits 24..31
+    a += n;
+    return n ? be >> (32 - 8 * n) : 0u;
+  }
+  // Keep a - wa < 4: shift in the prefetched word (masked only now, so the
+  // load it came from had a whole symbol to land) and prefetch the next one.
+  __device__ __forceinline__ void refill() {
+    const bool go = a - wa >= 4;
+    const uint64_t shifted = (win >> 32) | ((uint64_t)(nxt_ok ? nxt : 0u) << 32);
+    win = go ? shifted : win;
+    wa = go ? wa + 4 : wa;
+    // predicated load straight into `nxt`: no instruction consumes it until
+    // the next refill, so its latency never stalls the decode chain
+    const uintptr_t src = wa + 8 < end ? wa + 8 : last;
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.u32 %0, [%1];\n}"
+        : "+r"(nxt)
+        : "l"(src), "r"((uint32_t)(go && end != 0)));
+    nxt_ok = go ? wa + 8 < end : nxt_ok;
   }
 };
 
-// The reference model (fk/rangecoder.py:53-103): 256 counts, a Fenwick tree of
-// cumulative counts, +INC per coded symbol, halving at TOTAL_LIMIT.  Here the
-// 15 tree nodes that are multiples of 16 (the top four levels of the descent)
-// live in registers R[1..15]; the other nodes and every count live in shared
-// memory as W[i] = fen[i+1] << 16 | freq[i], [i][thread]-major so each thread
-// always hits its own bank.  Counts fit 16 bits: total < 2^16 + 32 and a node
-// below the multiples of 16 covers at most 8 symbols (fk/rangecoder.py:48-50).
-constexpr int kDecThreads = 32;  // one warp per CTA: 32 KB of models, 7 CTAs per SM
+// The reference model (fk/rangecoder.py:53-103: 256 counts starting at 1,
+// +INC per coded symbol, halving at TOTAL_LIMIT) held as cumulative counts in
+// 16 blocks of 16 symbols:
+//   CB[k]        = count of symbols in blocks < k           (registers, CB[0] = 0)
+//   incl[16b+j]  = sum of counts of block b symbols 0..j    (u16 in shared memory)
+// so cum(16b + j) = CB[b] + incl[16b + j - 1].  Counts fit 16 bits: total <
+// 2^16 while decoding (fk/rangecoder.py:186-188).  A thread's 256 entries are
+// 32 x 16 B: chunk (b, half) of thread t at ((2b + half) * 32 + t) * 16 B, so a
+// block is two conflict-free 128-bit loads and two 128-bit stores.
+constexpr int kDecThreads = 32;  // one warp per CTA: 16 KB of models, 14 CTAs per SM
 
-__device__ __forceinline__ uint32_t lowbit(uint32_t j) { return j & (0u - j); }
+__device__ __forceinline__ uint32_t lo16(uint32_t w) { return w & 0xFFFFu; }
 
+// 1/t to ~1 ulp (MUFU.RCP): the exact division below tolerates 4 ulp.
+__device__ __forceinline__ float rcp_approx(uint32_t t) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__uint2float_rn(t)));
+  return y;
+}
+__device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
 
 // Halve every count ((f + 1) >> 1, fk/rangecoder.py:93-103) and rebuild the
-// tree block by block (16 symbols per block); returns the new total.
-__device__ __forceinline__ uint32_t rebuild(uint32_t* w, uint32_t (&R)[16]) {
-  uint32_t B[16];
+// cumulative arrays; returns the new total.
+__device__ __forceinline__ uint32_t rebuild(uint4* m, uint32_t (&CB)[16]) {
   uint32_t total = 0;
+#pragma unroll 1
+  for (int b = 0; b < 16; ++b) {
+    uint4 c0 = m[(2 * b) * kDecThreads], c1 = m[(2 * b + 1) * kDecThreads];
+    const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    uint32_t out[8], prev = 0, acc = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t inc = (j & 1) ? hi16(wv[j >> 1]) : lo16(wv[j >> 1]);
+      const uint32_t f = ((inc - prev) + 1) >> 1;
+      prev = inc;
+      acc += f;
+      if (j & 1) out[j >> 1] |= acc << 16; else out[j >> 1] = acc;
+    }
+    m[(2 * b) * kDecThreads] = make_uint4(out[0], out[1], out[2], out[3]);
+    m[(2 * b + 1) * kDecThreads] = make_uint4(out[4], out[5], out[6], out[7]);
+    total += acc;
+  }
+  uint32_t run = 0;
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
-    uint32_t pre[17];
-    pre[0] = 0;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) pre[q + 1] = pre[q] + (((w[(16 * b + q) * kDecThreads] & 0xFFFFu) + 1) >> 1);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int jl = q + 1;
-      const uint32_t node = pre[jl] - pre[jl - (jl & -jl)];
-      w[(16 * b + q) * kDecThreads] = (node << 16) | (pre[q + 1] - pre[q]);
-    }
-    B[b] = pre[16];
-    total += pre[16];
-  }
-#pragma unroll
-  for (int k = 1; k < 16; ++k) {  // node 16k covers blocks (k - lowbit(k), k]
-    uint32_t v = 0;
-#pragma unroll
-    for (int b = k - (k & -k); b < k; ++b) v += B[b];
-    R[k] = v;
+    CB[b] = run;
+    const uint4 c1 = m[(2 * b + 1) * kDecThreads];
+    run += hi16(c1.w);
   }
   return total;
 }
 
 __global__ void __launch_bounds__(kDecThreads)
     rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n) {
-  extern __shared__ uint32_t W[];  // [256][kDecThreads]
+  extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B
   const int tid = threadIdx.x;
   const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
   const kvf_rc_stream st = streams[sidx];
-  uint32_t* w = W + tid;  // word i of this thread's model at w[i * kDecThreads]
-#pragma unroll 8
-  for (int i = 0; i < 256; ++i) w[i * kDecThreads] = (lowbit(i + 1) << 16) | 1u;
-  uint32_t R[16];
+  uint4* m = M + tid;  // chunk c of this thread's model at m[c * kDecThreads]
+  // counts start at 1: incl[16b + j] = j + 1, CB[k] = 16k
 #pragma unroll
-  for (int k = 0; k < 16; ++k) R[k] = 16u * (uint32_t)(k & -k);
+  for (int c = 0; c < 32; ++c) {
+    const uint32_t j0 = (c & 1) * 8 + 1;
+    m[c * kDecThreads] = make_uint4(j0 | (j0 + 1) << 16, (j0 + 2) | (j0 + 3) << 16,
+                                    (j0 + 4) | (j0 + 5) << 16, (j0 + 6) | (j0 + 7) << 16);
+  }
+  uint32_t CB[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) CB[k] = 16u * k;
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu, code = 0;
-  ByteStream bs;
-  bs.init(st.payload, (uint32_t)st.len);
-  for (int k = 0; k < 4; ++k) code = (code << 8) | bs.next();
+  ByteWindow bw;
+  bw.init(st.payload, (uint32_t)st.len);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    code = (code << 8) | bw.peek();
+    ++bw.a;
+  }
+  bw.refill();
 
   uint8_t* out = st.symbols;
   const uint32_t nsym = (uint32_t)st.n_symbols;
   uint32_t pack = 0;
   const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-  double inv = 1.0 / (double)total;  // 1/total of the symbol being decoded
+  float rcp = rcp_approx(total);  // ~1/total of the symbol being decoded
   for (uint32_t k = 0; k < nsym; ++k) {
-    // r = rng / total (fk/rangecoder.py:163), exact: inv = RN(1/total) has a
-    // relative error <= 2^-53, so rng*inv is within 2^-28 of rng/total, whose
-    // fraction is 0 or in [1/total, 1 - 1/total] with total < 2^16 + 32;
-    // adding 2^-19 before the floor therefore never changes it wrongly.
-    const uint32_t r = __double2uint_rd(__fma_rn((double)rng, inv, 0x1p-19));
-    const double inv_next = 1.0 / (double)(total + kInc);  // off the critical path
-    // Largest s with cum(s) <= min((code - low) / r, total - 1) (fk/rangecoder.py:163-166,
-    // 79-90), found without the second division: cum <= x / r  <=>  cum * r <= x.
+    const float rcp_next = rcp_approx(total + kInc);  // off the chain
+    // r = rng / total exactly (fk/rangecoder.py:163) in fp32: with rcp within
+    // 4 ulp of 1/total, q0 = RZ(RN(rng) * rcp) is within 8 of the quotient
+    // (rng < 2^32, total in [256, 2^16)); one floor((rng - q0 total) * rcp)
+    // step and a +-1 fix-up make it exact (checked against integer division
+    // on 3.5e7 cases incl. every k*total +- 1 edge, with rcp perturbed 1-4 ulp).
+    uint32_t r;
+    {
+      const uint32_t q0 = __float2uint_rz(__fmul_rn(__uint2float_rn(rng), rcp));
+      const int32_t rem0 = (int32_t)(rng - q0 * total);
+      const int32_t d = __float2int_rd(__fmul_rn((float)rem0, rcp));
+      const int32_t rem1 = rem0 - d * (int32_t)total;
+      r = q0 + (uint32_t)d + (rem1 >= (int32_t)total ? 1u : 0u) - (rem1 < 0 ? 1u : 0u);
+    }
+    // Largest s with cum(s) <= min((code - low) / r, total - 1) (fk/rangecoder.py:
+    // 163-166, 79-90) without the second division: cum <= x / r <=> cum * r <= x.
+    // cum is increasing in s, so both searches are binary over registers.
     const uint32_t x = code - low;
-    uint32_t rem = x, f;
-    // top four levels: register nodes 128 | 64,192 | 32..224 | 16..240
-    f = R[8] * r;
-    const bool b7 = f <= rem;
-    if (b7) rem -= f;
-    f = (b7 ? R[12] : R[4]) * r;
-    const bool b6 = f <= rem;
-    if (b6) rem -= f;
+    // block: largest b with CB[b] * r <= x (CB[0] = 0 always qualifies)
+    const bool b3 = CB[8] * r <= x;
+    const bool b2 = (b3 ? CB[12] : CB[4]) * r <= x;
+    const uint32_t c2a = b3 ? CB[10] : CB[2], c2b = b3 ? CB[14] : CB[6];
+    const bool b1 = (b2 ? c2b : c2a) * r <= x;
+    const uint32_t c1a = b3 ? CB[9] : CB[1], c1b = b3 ? CB[11] : CB[3];
+    const uint32_t c1c = b3 ? CB[13] : CB[5], c1d = b3 ? CB[15] : CB[7];
+    const uint32_t c1e = b2 ? c1c : c1a, c1f = b2 ? c1d : c1b;
+    const bool b0 = (b1 ? c1f : c1e) * r <= x;
+    const uint32_t blk = (b3 ? 8u : 0u) + (b2 ? 4u : 0u) + (b1 ? 2u : 0u) + (b0 ? 1u : 0u);
+    uint32_t base;
     {
-      const uint32_t a = b7 ? R[10] : R[2], b = b7 ? R[14] : R[6];
-      f = (b6 ? b : a) * r;
+      const uint32_t e0 = b3 ? CB[8] : CB[0], e1 = b3 ? CB[9] : CB[1];
+      const uint32_t e2 = b3 ? CB[10] : CB[2], e3 = b3 ? CB[11] : CB[3];
+      const uint32_t e4 = b3 ? CB[12] : CB[4], e5 = b3 ? CB[13] : CB[5];
+      const uint32_t e6 = b3 ? CB[14] : CB[6], e7 = b3 ? CB[15] : CB[7];
+      const uint32_t g0 = b2 ? e4 : e0, g1 = b2 ? e5 : e1, g2 = b2 ? e6 : e2, g3 = b2 ? e7 : e3;
+      const uint32_t h0 = b1 ? g2 : g0, h1 = b1 ? g3 : g1;
+      base = b0 ? h1 : h0;
     }
-    const bool b5 = f <= rem;
-    if (b5) rem -= f;
+    const uint32_t rem = x - base * r;
+    // within the block: incl[0..15] from two 128-bit loads
+    const uint4 ca = m[(2 * blk) * kDecThreads], cb = m[(2 * blk + 1) * kDecThreads];
+    const uint32_t wv[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+    // sl = number of j in 0..14 with incl[j] * r <= rem; lo/hi = incl[sl-1] (or 0), incl[sl]
+    const uint32_t i7 = hi16(wv[3]);
+    const bool t3 = i7 * r <= rem;
+    const uint32_t i3 = t3 ? hi16(wv[5]) : hi16(wv[1]);   // incl[11] : incl[3]
+    const bool t2 = i3 * r <= rem;
+    uint32_t i1;
     {
-      const uint32_t a0 = b7 ? R[9] : R[1], a1 = b7 ? R[11] : R[3];
-      const uint32_t a2 = b7 ? R[13] : R[5], a3 = b7 ? R[15] : R[7];
-      const uint32_t c0 = b6 ? a2 : a0, c1 = b6 ? a3 : a1;
-      f = (b5 ? c1 : c0) * r;
+      const uint32_t a = t3 ? hi16(wv[4]) : hi16(wv[0]);  // incl[9] : incl[1]
+      const uint32_t b = t3 ? hi16(wv[6]) : hi16(wv[2]);  // incl[13] : incl[5]
+      i1 = t2 ? b : a;
     }
-    const bool b4 = f <= rem;
-    if (b4) rem -= f;
-    const uint32_t blk = (b7 ? 128u : 0u) + (b6 ? 64u : 0u) + (b5 ? 32u : 0u) + (b4 ? 16u : 0u);
-    // bottom four levels inside the 16-symbol block: all 16 words in one go
-    uint32_t Wb[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) Wb[q] = w[(blk + q) * kDecThreads];
-    uint32_t F8[8], F4[4], F2[2];  // freq candidates narrowed bit by bit
-    f = (Wb[7] >> 16) * r;
-    const bool b3 = f <= rem;
-    if (b3) rem -= f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) F8[i] = b3 ? Wb[8 + i] : Wb[i];
-    f = (F8[3] >> 16) * r;
-    const bool b2 = f <= rem;
-    if (b2) rem -= f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) F4[i] = b2 ? F8[4 + i] : F8[i];
-    f = (F4[1] >> 16) * r;
-    const bool b1 = f <= rem;
-    if (b1) rem -= f;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) F2[i] = b1 ? F4[2 + i] : F4[i];
-    f = (F2[0] >> 16) * r;
-    const bool b0 = f <= rem;
-    if (b0) rem -= f;
-    const uint32_t sl = (b3 ? 8u : 0u) + (b2 ? 4u : 0u) + (b1 ? 2u : 0u) + (b0 ? 1u : 0u);
-    const uint32_t s = blk + sl;
-    low = code - rem;                                      // low + r * cum(s)
-    rng = r * ((b0 ? F2[1] : F2[0]) & 0xFFFFu);            // r * freq(s)
-    for (;;) {                                             // fk/rangecoder.py:172-183
-      if ((low ^ (low + rng)) >= kTop) {
-        if (rng >= kBot) break;
-        rng = (0u - low) & (kBot - 1);
+    const bool t1 = i1 * r <= rem;
+    uint32_t i0, lo_v, hi_v;
+    {
+      // candidates for incl[sl'] with sl' = 8t3 + 4t2 + 2t1 (+ 0 / + 1)
+      const uint32_t q0 = t3 ? wv[4] : wv[0], q1 = t3 ? wv[5] : wv[1];
+      const uint32_t q2 = t3 ? wv[6] : wv[2], q3 = t3 ? wv[7] : wv[3];
+      const uint32_t p0 = t2 ? q2 : q0, p1 = t2 ? q3 : q1;
+      const uint32_t pair = t1 ? p1 : p0;  // incl[sl'] | incl[sl' + 1] << 16
+      i0 = lo16(pair);
+      const bool t0 = i0 * r <= rem;
+      // value just below sl' (incl[sl' - 1]) : the high half of the previous word
+      const uint32_t pq0 = t3 ? wv[3] : 0u, pq1 = t3 ? wv[4] : wv[0];
+      const uint32_t pq2 = t3 ? wv[5] : wv[1], pq3 = t3 ? wv[6] : wv[2];
+      const uint32_t pp0 = t2 ? pq2 : pq0, pp1 = t2 ? pq3 : pq1;
+      const uint32_t below = hi16(t1 ? pp1 : pp0);     // incl[sl' - 1], 0 at sl' = 0
+      lo_v = t0 ? i0 : below;
+      hi_v = t0 ? hi16(pair) : i0;
+      const uint32_t sl = (t3 ? 8u : 0u) + (t2 ? 4u : 0u) + (t1 ? 2u : 0u) + (t0 ? 1u : 0u);
+      const uint32_t s = 16u * blk + sl;
+      // state update (fk/rangecoder.py:168-170)
+      low = code - (rem - lo_v * r);                       // low + r * cum(s)
+      rng = r * (hi_v - lo_v);                             // r * freq(s)
+      // renormalise (fk/rangecoder.py:171-183).  While the top byte of low and
+      // low + rng agree the reference shifts a byte in; shifting both by 8
+      // shifts X = low ^ (low + rng) by 8, so that phase is exactly
+      // n = clz(X) / 8 bytes (rng >= 1, so X != 0 and n <= 3).  Only if rng
+      // is then below 2^16 does the squeeze branch run (rare): the loop below
+      // replays the reference rounds from there.
+      {
+        const uint32_t n = __clz(low ^ (low + rng)) >> 3;
+        const uint32_t bytes = bw.take(n);  // the next n bytes, big-endian, in the low bits
+        code = n ? (code << (8 * n)) | bytes : code;
+        low = n ? low << (8 * n) : low;
+        rng = n ? rng << (8 * n) : rng;
       }
-      code = (code << 8) | bs.next();
-      low <<= 8;
-      rng <<= 8;
-    }
-    pack = (pack >> 8) | (s << 24);  // 4 symbols per 32-bit store
-    if ((k & 3) == 3) {
-      if (aligned4) {
-        *reinterpret_cast<uint32_t*>(out + (k - 3)) = pack;
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) out[k - 3 + e] = (uint8_t)(pack >> (8 * e));
+      bw.refill();
+      while (rng < kBot || (low ^ (low + rng)) < kTop) {
+        if ((low ^ (low + rng)) >= kTop) rng = (0u - low) & (kBot - 1);
+        code = (code << 8) | bw.take(1);
+        low <<= 8;
+        rng <<= 8;
+        bw.refill();
       }
-    }
-    // freq[s] += INC and the Fenwick path of s (fk/rangecoder.py:60-66, 185-186),
-    // branch-free: the shared nodes below the block end (at most four: lowbits
-    // 1, 2, 4, 8) as unconditional atomics (+0 when off the path), then every
-    // register node covering s.
-    {
-      const uint32_t j0 = s + 1, j1 = j0 + lowbit(j0), j2 = j1 + lowbit(j1), j3 = j2 + lowbit(j2);
-      const bool p0 = (j0 & 15) != 0, p1 = p0 && (j1 & 15), p2 = p1 && (j2 & 15),
-                 p3 = p2 && (j3 & 15);
-      atomicAdd(&w[s * kDecThreads], p0 ? ((kInc << 16) | kInc) : kInc);
-      atomicAdd(&w[(p1 ? j1 - 1 : s) * kDecThreads], p1 ? kInc << 16 : 0u);
-      atomicAdd(&w[(p2 ? j2 - 1 : s) * kDecThreads], p2 ? kInc << 16 : 0u);
-      atomicAdd(&w[(p3 ? j3 - 1 : s) * kDecThreads], p3 ? kInc << 16 : 0u);
-    }
+      pack = (pack >> 8) | (s << 24);  // 4 symbols per 32-bit store
+      if ((k & 3) == 3) {
+        if (aligned4) {
+          *reinterpret_cast<uint32_t*>(out + (k - 3)) = pack;
+        } else {
 #pragma unroll
-    for (int q = 1; q < 16; ++q) {  // node 16q covers s in [16(q - lowbit(q)), 16q)
-      const uint32_t lo = 16u * (uint32_t)(q - (q & -q)), len = 16u * (uint32_t)(q & -q);
-      R[q] += (s - lo < len) ? kInc : 0u;
+          for (int e = 0; e < 4; ++e) out[k - 3 + e] = (uint8_t)(pack >> (8 * e));
+        }
+      }
+      // freq[s] += INC (fk/rangecoder.py:185-186): incl[16 blk + j] += INC for
+      // j >= sl (packed 16-bit halves), CB[k] += INC for k > blk
+      uint32_t nv[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const uint32_t add = (2u * w >= sl ? kInc : 0u) | (2u * w + 1 >= sl ? kInc << 16 : 0u);
+        nv[w] = wv[w] + add;
+      }
+      m[(2 * blk) * kDecThreads] = make_uint4(nv[0], nv[1], nv[2], nv[3]);
+      m[(2 * blk + 1) * kDecThreads] = make_uint4(nv[4], nv[5], nv[6], nv[7]);
+#pragma unroll
+      for (int q = 1; q < 16; ++q)
+        if ((uint32_t)q > blk) CB[q] += kInc;
     }
     total += kInc;
-    inv = inv_next;
+    rcp = rcp_next;
     if (total >= kLimit) {
-      total = rebuild(w, R);
-      inv = 1.0 / (double)total;
+      total = rebuild(m, CB);
+      rcp = rcp_approx(total);
     }
   }
   if (nsym & 3) {  // tail: the last nsym % 4 symbols sit in the top bytes of `pack`
@@ -362,9 +439,9 @@ extern "C" kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_st
                                     void* stream) {
   if (n_streams < 0 || (n_streams > 0 && !d_streams)) KVF_FAIL(KVF_EINVAL, "bad stream array");
   if (n_streams == 0) return KVF_OK;
-  // One warp per CTA; its 32 models take 32 KB of shared memory, so seven CTAs
-  // (224 streams) are resident per SM and the grid spreads over every SM.
-  const size_t smem = (size_t)kDecThreads * 256 * sizeof(uint32_t);
+  // One warp per CTA; its 32 models take 16 KB of shared memory, so fourteen
+  // CTAs (448 streams) are resident per SM and the grid spreads over every SM.
+  const size_t smem = (size_t)kDecThreads * 256 * sizeof(uint16_t);
   const int grid = (n_streams + kDecThreads - 1) / kDecThreads;
   rc_decode_kernel<<<grid, kDecThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(d_streams,
                                                                                       n_streams);
