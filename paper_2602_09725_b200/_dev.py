@@ -29,7 +29,11 @@ def stream_ptr(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
 
 
 def to_device(x, dtype: torch.dtype | None = None) -> torch.Tensor:
-    """numpy / CPU tensor / CUDA tensor -> CUDA tensor (explicit H2D for host data)."""
+    """numpy / CPU tensor / CUDA tensor -> CUDA tensor.
+
+    Host data is staged through pinned memory and copied asynchronously on the
+    current stream (stream-ordered for every later use; a pageable copy would
+    block the host until all work already queued on the stream finished)."""
     if isinstance(x, np.ndarray):
         x = torch.from_numpy(np.ascontiguousarray(x))
     if not isinstance(x, torch.Tensor):
@@ -37,7 +41,8 @@ def to_device(x, dtype: torch.dtype | None = None) -> torch.Tensor:
     if dtype is not None and x.dtype != dtype:
         x = x.to(dtype)
     if not x.is_cuda:
-        x = x.to(device(), non_blocking=False)
+        x = x.contiguous()
+        x = (x if x.is_pinned() else x.pin_memory()).to(device(), non_blocking=True)
     return x
 
 

@@ -258,9 +258,10 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
         ch_arr = np.concatenate(chain_parts) if chain_parts else np.zeros(1, _CHAIN_DTYPE)
         k_rc = sum(len(x) for x in rc_parts)
         chains = ch_arr if chain_parts else []
-        d_rc = torch.from_numpy(rc.view(np.uint8)).to(dev)
-        d_planes = torch.from_numpy(flat.view(np.uint8)).to(dev)
-        d_chains = torch.from_numpy(ch_arr.view(np.uint8)).to(dev)
+        # descriptor arrays via pinned memory: asynchronous, never a host sync
+        d_rc, d_planes, d_chains = (
+            torch.from_numpy(a.view(np.uint8)).pin_memory().to(dev, non_blocking=True)
+            for a in (rc, flat, ch_arr))
         sp = _dev.stream_ptr(s)
         _lib.call("kvf_rc_decode", _dev.ptr(d_rc), k_rc, sp)
         _lib.call("kvf_kvfc_reconstruct", _dev.ptr(d_planes), _dev.ptr(d_chains), len(chains), sp)

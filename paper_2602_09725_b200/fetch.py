@@ -169,7 +169,7 @@ def _mem_for(mem, cache_id):
 def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=None,
                         initial_active="R1080", timeout_s=30.0, on_chunk=None, *, mem=None,
                         scales_dtype_out=None, real_layers=None, depth=32, max_batch=32,
-                        fetch_fn=None, workers=2):
+                        fetch_fn=None, workers=1):
     """Fetch chunks from a live server and decode them on the GPU as they arrive.
 
     ``chunks``: list of (cache_id, chunk_index).  Without ``mem`` each chunk is
@@ -212,6 +212,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
             else:
                 conts = [NS.container_of(meta, b"") for _, meta, _ in items]
                 frames, held = codec.decode_batch([p for _, _, p in items], stream=gpu_stream)
+                t_dec = time.monotonic()
                 units = []
                 with claim_lock:  # claim every unit, then describe (pools may grow)
                     for cont, fr, (_, meta, _) in zip(conts, frames, items):
@@ -222,6 +223,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                                                   3 * cont.layer_triplet_index,
                                                   cont.token_start, sc, real_layers))
                     restore_units(units, stream=gpu_stream)
+                t_res = time.monotonic()
                 results = [{"tokens_written": u.tokens_written} for u in units]
             done = torch.cuda.Event()
             done.record(gpu_stream)
@@ -229,9 +231,11 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
         gpu_stream.synchronize()
         t1 = time.monotonic()
         with claim_lock:
+            host = {} if mem is None else {"host_decode_s": t_dec - t0,
+                                           "host_restore_s": t_res - t_dec}
             for rec, _, _ in items:
                 rec.update(decode_start=t0 - base, decode_end=t1 - base, tau_dec=t1 - t0,
-                           batch=len(items))
+                           batch=len(items), **host)
             if state["dec_end"] is not None:
                 bubble = max(0.0, t0 - base - state["dec_end"])
                 items[0][0]["bubble"] = bubble

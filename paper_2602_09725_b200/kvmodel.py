@@ -238,7 +238,8 @@ class PagedMemory:
         return self._table
 
     def _map_pages(self, first_page: int, last_page: int):
-        need = [p for p in range(first_page, last_page + 1) if p not in self.pages]
+        pages = self.pages
+        need = [p for p in range(first_page, last_page + 1) if p not in pages]
         if need:
             if len(self._free) < len(need):
                 self._ensure_blocks(self._cap_blocks + len(need) - len(self._free))
@@ -270,16 +271,20 @@ class PagedMemory:
         elif (self.H, self.D) != (H, D):
             raise ValueError(f"slot shape {(H, D)} differs from the cache's {(self.H, self.D)}")
         self._grow_marks(int(tokens.max()) + 1, max(layers) + 1)
-        hit = self._written[np.ix_(tokens, layers)]
+        lo, hi = int(tokens.min()), int(tokens.max())
+        # a whole chunk is a contiguous token range: slice instead of fancy-index
+        rows = slice(lo, hi + 1) if hi - lo + 1 == len(tokens) else tokens
+        idx = (rows, layers) if isinstance(rows, slice) else np.ix_(tokens, layers)
+        hit = self._written[idx]
         if hit.any():
             ti, li = np.argwhere(hit)[0]
             raise ConflictError(
                 f"slot (token={int(tokens[ti])}, layer={layers[li]}) already written")
         self._ensure_layers(max(layers) + 1)
         bs = self.page_size_tokens
-        self._map_pages(int(tokens.min()) // bs, int(tokens.max()) // bs)
-        self._written[np.ix_(tokens, layers)] = True
-        self._present[np.ix_(tokens, layers)] = True
+        self._map_pages(lo // bs, hi // bs)
+        self._written[idx] = True
+        self._present[idx] = True
         self.allocated_bytes += len(tokens) * len(layers) * self.slot_bytes
         self.peak_bytes = max(self.peak_bytes, self.allocated_bytes)
 

@@ -16,6 +16,8 @@ from __future__ import annotations
 
 import hashlib
 
+import numpy as np
+
 import torch
 
 from . import _dev, _lib
@@ -155,9 +157,13 @@ class FramePlan:
         return out
 
     def tokens_in_frames(self, first, n):
-        """Chunk token indices held by frames [first, first+n) (sorted)."""
-        toks = [i for f in range(first, first + n) for i, _, _ in self.frame_slots(f)]
-        return sorted(toks)
+        """Chunk token indices held by frames [first, first+n) (sorted int64 array)."""
+        if first <= 0 and first + n >= self.frame_count:
+            return np.arange(self.T, dtype=np.int64)       # the whole chunk
+        f = np.arange(first, first + n, dtype=np.int64)[:, None]
+        slot = np.arange(self.tiles_per_frame, dtype=np.int64)[None, :]
+        i = ((f // self.F) * self.tiles_per_frame + slot) * self.F + f % self.F
+        return np.sort(i[i < self.T])
 
     def digest(self):
         key = (f"{self.T}/{self.F}/{self.K}/{self.tiles_per_frame}/"

@@ -121,3 +121,16 @@ def test_select_resolution_and_bandwidth():
             deltas.append((abs(table.size_bytes(r) * 8 / (bw * 1e9) - 0.1 - pen), r))
         best = min(d for d, _ in deltas)
         assert got == [r for d, r in deltas if d == best][-1]
+
+
+@pytest.mark.parametrize("res", L.RESOLUTION_ORDER)
+@pytest.mark.parametrize("T", [1, 7, 65, 999, 10000])
+def test_tokens_in_frames_matches_frame_slots(res, T):
+    """The vectorised slot enumeration restore claims with equals the
+    reference's per-frame frame_slots walk (fk/layout.py:203-212)."""
+    plan = L.plan_inter_frame(T, res, L.identity_layout(8, 32), 4)
+    for first, n in [(0, plan.frame_count), (0, 1), (plan.frame_count - 1, 1),
+                     (plan.frame_count // 2, plan.frame_count - plan.frame_count // 2),
+                     (min(4, plan.frame_count - 1), min(4, plan.frame_count - min(4, plan.frame_count - 1)))]:
+        want = sorted(i for f in range(first, first + n) for i, _, _ in plan.frame_slots(f))
+        assert list(plan.tokens_in_frames(first, n)) == want

@@ -129,6 +129,9 @@ def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
         "decode_batches": len({r["decode_start"] for r in recs}),
         "max_batch": max(r.get("batch", 1) for r in recs),
         "total_bubble_s": round(tl.total_bubble, 4),
+        "host_decode_s": round(sum(r.get("host_decode_s", 0) for r in {r["decode_start"]: r for r in recs}.values()), 4),
+        "host_restore_s": round(sum(r.get("host_restore_s", 0) for r in {r["decode_start"]: r for r in recs}.values()), 4),
+        "gpu_busy_s": round(sum(r["tau_dec"] for r in {r["decode_start"]: r for r in recs}.values()), 4),
         "sampled_slots_mismatch": check(mems, qs, Lyr, args.tokens),
         "setup_pack_s": round(setup_s, 1),
     }
@@ -141,6 +144,7 @@ def main():
     ap.add_argument("--rates", default="10,25,100,0", help="Gbps; 0 = unthrottled loopback")
     ap.add_argument("--res", default="R240,R1080")
     ap.add_argument("--dir", default=None)
+    ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--link", default="model", choices=["model", "tcp"],
                     help="model: constant-rate arrival replay; tcp: live loopback server")
     args = ap.parse_args()
@@ -168,7 +172,7 @@ def main():
             mems = new_mems(qs, args.tokens, Lyr, H, D)
             torch.cuda.synchronize()
             tl = FE.live_fetch_pipeline(None, chunks, None, f"fixed:{res}", mem=mems,
-                                        real_layers=Lyr, fetch_fn=link)
+                                        real_layers=Lyr, fetch_fn=link, workers=args.workers)
             emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, "modelled constant-rate link")
             del mems, link
             torch.cuda.empty_cache()
