@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fetch", action="store_true", help="skip the fetch-to-ready leg")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--cpu-units", type=int, default=2, help="sample units per CPU worker")
     return ap.parse_args()
 
@@ -469,10 +470,15 @@ def main():
 
     from paper_2602_09725_b200 import shard
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; --dist-backend gloo with more ranks than GPUs lets the
+    # N>1 path (sharding, max/sum over ranks) run on a single-GPU box for checks
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     d = dist if world > 1 else None
 
     w = Workload(args, dev, rank, world)

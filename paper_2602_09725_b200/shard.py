@@ -107,8 +107,9 @@ def _reduce(value: float, op: str, dist=None, device=None) -> float:
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
         return float(value)
     import torch
-    t = torch.tensor([float(value)], dtype=torch.float64,
-                     device=device if device is not None else "cpu")
+    if device is None or dist.get_backend() == "gloo":
+        device = "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=getattr(dist.ReduceOp, op))
     return float(t.item())
 
