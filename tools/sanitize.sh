@@ -1,0 +1,13 @@
+#!/bin/bash
+# compute-sanitizer memcheck + racecheck over the GPU parity/codec tests.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+python -m paper_2602_09725_b200.build > gpurun_out/build.txt 2>&1 || { cat gpurun_out/build.txt; exit 1; }
+SEL='test_restore_paged_matches_oracle or test_fused_pack_matches_oracle or test_golden_streams_decode or test_random_sequences_batched or test_encode_bit_exact or test_restore_batch_mixed or test_pack_paged_source'
+for tool in memcheck racecheck; do
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
+      python -m pytest tests/test_gpu_parity.py tests/test_gpu_codec.py -q -x -k "$SEL" \
+      > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "$tool rc=$?" | tee -a gpurun_out/sanitize_$tool.txt
+  grep -E "ERROR SUMMARY|passed|failed" gpurun_out/sanitize_$tool.txt | tail -3
+done
