@@ -163,3 +163,46 @@ def test_fetch_errors(tmp_path):
             NS.fetch_chunk(addr, b"\x00" * 16, 0, 7)
     finally:
         handle.close()
+
+
+def test_pipelined_fetch_batches_k_and_v_into_paged_bf16(tmp_path):
+    """The batched pipeline (several chunks per decode launch, two caches) with a
+    replayed link: every K and V slot equals dequantize() of the packed codes."""
+    cfg = L.identity_layout(8, 32)
+    store_chunks, qs = [], {}
+    for kv_i in range(2):
+        cid = bytes([0x50 + kv_i]) * 16
+        q, _ = _q(dict(kind="synthetic", T=300, L=5, H=8, D=32, s=0.9, seed=11 + kv_i, c=0.3,
+                       group_size=64, bf16=True))
+        qp = KV.QuantizedKV(torch.cat([q.values, torch.zeros_like(q.values[:, :1])], 1),
+                            torch.cat([q.scales, torch.ones_like(q.scales[:1])], 0), 64)
+        qs[cid] = q
+        for j in range(2):
+            for c, t0 in enumerate((0, 128, 256)):
+                tc = min(128, 300 - t0)
+                slab = KV.QuantizedKV(qp.values[t0:t0 + tc, 3 * j:3 * j + 3],
+                                      qp.scales[3 * j:3 * j + 3], 64)
+                cont = C.pack_chunk(slab, cfg, ["R240"], cache_id=cid, chunk_index=10 * j + c,
+                                    token_start=t0, layer_triplet_index=j)
+                (tmp_path / C.container_filename(cid, 10 * j + c)).write_bytes(cont.to_bytes())
+                store_chunks.append((cid, 10 * j + c))
+    store = NS.ChunkStore(str(tmp_path), preload=True)
+    staged = {key: store.lookup(key[0], key[1], L.RESOLUTION_CODE["R240"]) for key in store_chunks}
+
+    def replay(address, cache_id, chunk_index, resolution, timeout_s=30.0, alloc=None):
+        meta, payload = staged[(bytes(cache_id), chunk_index)]
+        buf = alloc(len(payload))
+        buf.numpy()[:] = np.frombuffer(payload, np.uint8)
+        return buf, meta, 1e-3
+
+    mems = {cid: KV.PagedMemory(16, dtype=torch.bfloat16) for cid in qs}
+    tl = FE.live_fetch_pipeline(None, store_chunks, None, "fixed:R240", mem=mems, real_layers=5,
+                                fetch_fn=replay, max_batch=4)
+    assert len(tl.records) == len(store_chunks)
+    assert max(r["batch"] for r in tl.records) >= 1
+    for cid, q in qs.items():
+        deq = KV.dequantize(q, torch.bfloat16).data
+        for t in (0, 127, 128, 255, 256, 299):
+            for l in range(5):
+                assert torch.equal(mems[cid].read(t, l), deq[t, l].reshape(-1)), (cid, t, l)
+        assert mems[cid].read(0, 5) is None          # pad layer never written
