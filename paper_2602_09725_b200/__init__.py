@@ -6,10 +6,13 @@ names and entry points:
   kvmodel   - KVCache, QuantizedKV, quantize/dequantize, PagedMemory (GPU)
   layout    - LayoutConfig, FramePlan, assemble_frames/disassemble_frames (GPU)
   codec     - KVFC frame codec: GPU range decoder/encoder + predictor
+  rangecoder- encode_bytes / decode_bytes on the GPU (fk/rangecoder.py)
   container - KVFC chunk container: pack_chunk / unpack_chunk
   restore   - restore_stream / restore_chunk_wise / restore_frames (GPU, fused dequant)
   netstore  - chunk server + wire protocol (host transport, reference-compatible)
   fetch     - live_fetch_pipeline: network receive || GPU decode + restore
+  fetchsim  - the fk/fetchsim.py names of the above (restore_stream, policy helpers)
+  shard     - (request, K/V, triplet, chunk) units and their assignment to GPUs
 
 Every data-path call goes through libkvf.so (include/kvf.h); there is no CPU
 fallback — importing works without a GPU, calling a kernel does not.
