@@ -521,6 +521,15 @@ def main():
                "kind": "port",
                "sample": f"{cores} processes x {args.cpu_units} units of {CHUNK} tokens x 3 "
                          f"layers: oracle disassemble_frames + dequantize + bf16 + paged scatter"}
+        if fetch is not None:  # the same host's cores decoding the context's KVFC streams
+            sym, dwall, dcores = bench_cpu.run("decode", units_per_worker=1, T=CHUNK, H=H, D=D,
+                                               res=args.res, lay=lay)
+            rate = sym / dwall
+            fetch["cpu_decode"] = {
+                "msym_per_s": round(rate / 1e6, 1), "cores": dcores, "kind": "port",
+                "est_context_decode_s": round(fetch["frame_bytes"] / rate, 2),
+                "sample": f"{dcores} processes x 8 {args.res} frames: C restatement of "
+                          f"decode_frames (fk/codec.py:155-211, fk/rangecoder.py:146-189)"}
 
     if rank == 0:
         clocks = clk.summary()

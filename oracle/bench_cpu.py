@@ -6,7 +6,8 @@ with the oracle — the numpy restatement of the reference — and times the
 reference's restore transform on it: disassemble_frames (fk/layout.py:261-271)
 -> dequantize (fk/kvmodel.py:147-152) -> bf16 -> paged scatter through a block
 table (PagedMemory.page_write, fk/kvmodel.py:216-229), or the pack transform:
-quantize (fk/kvmodel.py:127-144) + assemble_frames (fk/layout.py:234-258).
+quantize (fk/kvmodel.py:127-144) + assemble_frames (fk/layout.py:234-258), or
+the KVFC decode of a sample stream (the C restatement of decode_frames).
 """
 
 from __future__ import annotations
@@ -69,6 +70,22 @@ def pack_worker(args):
     return total_t, total_e
 
 
+def decode_worker(args):
+    """Time the reference KVFC decode (oracle C restatement of decode_frames,
+    fk/codec.py:155-211 + fk/rangecoder.py:146-189) on a sample stream."""
+    seed, units, T, H, D, res, lay, gs = args
+    _, _, _, plan, frames = _sample(seed, T, H, D, res, lay, gs)
+    n = min(8, plan.frame_count)
+    bs = ref.encode_frames(frames[:n], plan.F)
+    total_t, total_e = 0.0, 0
+    for _ in range(units):
+        t0 = time.perf_counter()
+        out = ref.decode_frames(bs)
+        total_t += time.perf_counter() - t0
+        total_e += out.size
+    return total_t, total_e
+
+
 def run(kind="restore", workers=None, units_per_worker=2, T=10000, H=8, D=128, res="R1080",
         lay=(8, 128, 1, 8, 1, 128), gs=128):
     """Run `workers` processes concurrently; returns (elements, wall seconds, cores).
@@ -77,7 +94,7 @@ def run(kind="restore", workers=None, units_per_worker=2, T=10000, H=8, D=128, r
     total elements / the slowest worker's timed seconds (all run concurrently).
     """
     workers = workers or os.cpu_count() or 1
-    fn = restore_worker if kind == "restore" else pack_worker
+    fn = {"restore": restore_worker, "pack": pack_worker, "decode": decode_worker}[kind]
     jobs = [(w + 1, units_per_worker, T, H, D, res, tuple(lay), gs) for w in range(workers)]
     if workers == 1:
         res_list = [fn(jobs[0])]
