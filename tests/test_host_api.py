@@ -134,3 +134,18 @@ def test_tokens_in_frames_matches_frame_slots(res, T):
                      (min(4, plan.frame_count - 1), min(4, plan.frame_count - min(4, plan.frame_count - 1)))]:
         want = sorted(i for f in range(first, first + n) for i, _, _ in plan.frame_slots(f))
         assert list(plan.tokens_in_frames(first, n)) == want
+
+
+def test_b200_lookup_table_and_adaptive_choice():
+    """The measured B200 decode table (data/b200.json, reference table format
+    fk/data/h20.json) loads, validates, and drives Alg. 1 (select_resolution,
+    fk/fetchsim.py:154-169): fast links pick the short-stream class whose GPU
+    decode hides under the transfer; a slow link can afford R1080."""
+    from paper_2602_09725_b200 import fetch as FE
+    t = FE.default_table()
+    assert t.P >= 1 and set(t.decode_s) == set(L.RESOLUTION_ORDER)
+    assert t.tau_dec("R240", 1) < t.tau_dec("R1080", 1)   # more, shorter streams decode faster
+    assert FE.LookupTable.from_json(t.to_json()).decode_s == t.decode_s
+    assert FE.select_resolution(100.0, 1, "R1080", t) == "R240"
+    assert FE.select_resolution(10.0, 1, "R1080", t) == "R240"
+    assert FE.select_resolution(1.0, 1, "R1080", t) == "R1080"

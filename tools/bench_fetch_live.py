@@ -74,17 +74,19 @@ class ModelLink:
         self.store, self.rate = store, rate_gbps * 1e9
         self.t0, self.sent, self.pinned = None, 0, {}
 
-    def stage(self, chunks, code):
-        for cid, idx in chunks:
-            meta, payload = self.store.lookup(cid, idx, code)
-            t = torch.frombuffer(bytearray(payload), dtype=torch.uint8).pin_memory()
-            self.pinned[(cid, idx)] = (meta, t)
+    def stage(self, chunks, codes):
+        for code in codes:
+            for cid, idx in chunks:
+                meta, payload = self.store.lookup(cid, idx, code)
+                t = torch.frombuffer(bytearray(payload), dtype=torch.uint8).pin_memory()
+                self.pinned[(cid, idx, code)] = (meta, t)
 
     def __call__(self, address, cache_id, chunk_index, resolution, timeout_s=30.0, alloc=None):
         now = time.monotonic()
         if self.t0 is None:
             self.t0 = now
-        meta, t = self.pinned[(bytes(cache_id), chunk_index)]
+        code = resolution if isinstance(resolution, int) else L.RESOLUTION_CODE[resolution]
+        meta, t = self.pinned[(bytes(cache_id), chunk_index, code)]
         self.sent += t.numel()
         arrive = self.t0 + self.sent * 8 / self.rate
         if arrive > now:
@@ -128,6 +130,8 @@ def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
         "tail_after_last_byte_s": round(tl.ttft - last_rx, 4),
         "decode_batches": len({r["decode_start"] for r in recs}),
         "max_batch": max(r.get("batch", 1) for r in recs),
+        "chosen": {k: sum(1 for r in recs if r["resolution"] == k)
+                   for k in sorted({r["resolution"] for r in recs})},
         "total_bubble_s": round(tl.total_bubble, 4),
         "host_decode_s": round(sum(r.get("host_decode_s", 0) for r in {r["decode_start"]: r for r in recs}.values()), 4),
         "host_restore_s": round(sum(r.get("host_restore_s", 0) for r in {r["decode_start"]: r for r in recs}.values()), 4),
@@ -156,22 +160,25 @@ def main():
     setup_s = time.perf_counter() - t0
     store = NS.ChunkStore(root)
     ctx = mp.get_context("spawn")
-    for res in resolutions:
-        code = L.RESOLUTION_CODE[res]
-        coded = sum(store.index[(cid, idx)]["entries"][code][1] for cid, idx in chunks)
+    for res in resolutions + (["adaptive"] if args.link == "model" and len(resolutions) == 4 else []):
+        codes = ([L.RESOLUTION_CODE[r] for r in resolutions] if res == "adaptive"
+                 else [L.RESOLUTION_CODE[res]])
+        code = codes[0]
+        coded = sum(store.index[(cid, idx)]["entries"][code][1] for cid, idx in chunks)  # fixed classes
+        policy = "adaptive" if res == "adaptive" else f"fixed:{res}"
         # untimed warm-up: pins the receive pool, grows the allocator, loads kernels
         link = ModelLink(store, 1000.0)
-        link.stage(chunks, code)
-        FE.live_fetch_pipeline(None, chunks, None, f"fixed:{res}",
+        link.stage(chunks, codes)
+        FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=10.0,
                                mem=new_mems(qs, args.tokens, Lyr, H, D), real_layers=Lyr,
                                fetch_fn=link)
         del link
         for rate in [float(r) for r in args.rates.split(",")] if args.link == "model" else []:
             link = ModelLink(store, rate)
-            link.stage(chunks, code)
+            link.stage(chunks, codes)
             mems = new_mems(qs, args.tokens, Lyr, H, D)
             torch.cuda.synchronize()
-            tl = FE.live_fetch_pipeline(None, chunks, None, f"fixed:{res}", mem=mems,
+            tl = FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=rate, mem=mems,
                                         real_layers=Lyr, fetch_fn=link, workers=args.workers)
             emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, "modelled constant-rate link")
             del mems, link
