@@ -33,7 +33,13 @@ _PLANE_DTYPE = np.dtype([("symbols", "<u8"), ("modes", "<u8"), ("out", "<u8"),
                          ("out_pitch", "<i8")])
 _CHAIN_DTYPE = np.dtype([("first", "<i4"), ("count", "<i4"), ("height", "<i4"),
                          ("width", "<i4")])
+_RESID_DTYPE = np.dtype([("cur", "<u8"), ("prev", "<u8"), ("pitch", "<i8"), ("symbols", "<u8"),
+                         ("modes", "<u8"), ("height", "<i4"), ("width", "<i4")])
+_PIECE_DTYPE = np.dtype([("src", "<u8"), ("dst_off", "<i8"), ("len", "<i8"), ("pack_bits", "<i4"),
+                         ("reserved_", "<i4")])
 assert _RC_DTYPE.itemsize == C.sizeof(_lib.kvf_rc_stream)
+assert _RESID_DTYPE.itemsize == C.sizeof(_lib.kvf_resid_plane)
+assert _PIECE_DTYPE.itemsize == C.sizeof(_lib.kvf_piece)
 assert _PLANE_DTYPE.itemsize == C.sizeof(_lib.kvf_recon_plane)
 assert _CHAIN_DTYPE.itemsize == C.sizeof(_lib.kvf_recon_chain)
 
@@ -288,12 +294,19 @@ def decode_frames(bs, cfg: CodecConfig, on_frame, stats=None):
     return fr.shape[0]
 
 
+def _to_dev_struct(arr: np.ndarray, dev) -> torch.Tensor:
+    """numpy structured array -> device bytes (pinned, asynchronous)."""
+    return torch.from_numpy(arr.view(np.uint8)).pin_memory().to(dev, non_blocking=True)
+
+
 def encode_batch(frame_sets, gops, stream=None):
     """Encode many [n, 3, h, w] uint8 frame tensors on the GPU (fk/codec.py:93-128).
 
     Returns a list of Bitstream.  Launches: residual/mode kernel, range
     encoder (one thread per (frame, plane) stream), one D2H of the coded
-    lengths, the gather kernel, one D2H of all streams.
+    lengths and modes, the gather kernel, one D2H of all streams.  Host work
+    (descriptors, stream layout fk/codec.py:16-20, header fields) is
+    vectorised over planes.
     """
     dev = _dev.device()
     sets = [_dev.to_device(f, torch.uint8) for f in frame_sets]
@@ -303,92 +316,93 @@ def encode_batch(frame_sets, gops, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     with torch.cuda.stream(s):
         sets = [f if f.stride(3) == 1 and f.stride(2) == f.shape[3] else f.contiguous() for f in sets]
-        geo = []
-        n_planes = 0
-        sym_total = 0
-        mode_total = 0
+        geo, n_planes, sym_total, mode_total = [], 0, 0, 0
         for f in sets:
             n, _, h, w = f.shape
             bh, bw = -(-h // BLOCK), -(-w // BLOCK)
-            geo.append((n, h, w, bh, bw, sym_total, mode_total, n_planes))
+            hw4 = -(-h * w // 4) * 4
+            geo.append((n, h, w, bh, bw, hw4, sym_total, mode_total, n_planes))
             n_planes += 3 * n
-            sym_total += 3 * n * h * w
+            sym_total += 3 * n * hw4
             mode_total += 3 * n * bh * bw
         symbols = torch.empty(max(sym_total, 1), dtype=torch.uint8, device=dev)
         modes = torch.zeros(max(mode_total, 1), dtype=torch.uint8, device=dev)
-        cap = [2 * h * w + 16 for (n, h, w, *_r) in geo for _ in range(3 * n)]
-        cap_off = np.concatenate([[0], np.cumsum(cap)]).astype(np.int64) if cap else np.zeros(1, np.int64)
+        rp = np.zeros(max(n_planes, 1), _RESID_DTYPE)
+        rc = np.zeros(max(n_planes, 1), _RC_DTYPE)
+        caps, max_blocks = [], 0
+        for f, gop, (n, h, w, bh, bw, hw4, s0, m0, k0) in zip(sets, gops, geo):
+            max_blocks = max(max_blocks, bh * bw)
+            k = np.arange(3 * n, dtype=np.int64)
+            fi, p = k // 3, k % 3
+            sl = slice(k0, k0 + 3 * n)
+            rp["cur"][sl] = f.data_ptr() + fi * f.stride(0) + p * f.stride(1)
+            rp["prev"][sl] = np.where(fi % gop != 0, f.data_ptr() + (fi - 1) * f.stride(0)
+                                      + p * f.stride(1), 0)
+            rp["pitch"][sl] = f.stride(2)
+            rp["symbols"][sl] = symbols.data_ptr() + s0 + k * hw4
+            rp["modes"][sl] = modes.data_ptr() + m0 + k * bh * bw
+            rp["height"][sl], rp["width"][sl] = h, w
+            rc["symbols"][sl] = rp["symbols"][sl]
+            rc["n_symbols"][sl] = h * w
+            caps.append(np.full(3 * n, 2 * h * w + 16, np.int64))
+        cap = np.concatenate(caps) if caps else np.zeros(0, np.int64)
+        cap_off = np.concatenate([[0], np.cumsum(cap)]).astype(np.int64)
         payload = torch.empty(max(int(cap_off[-1]), 1), dtype=torch.uint8, device=dev)
         out_len = torch.zeros(max(n_planes, 1), dtype=torch.int64, device=dev)
-        rp = (_lib.kvf_resid_plane * max(1, n_planes))()
-        rc = (_lib.kvf_rc_stream * max(1, n_planes))()
-        max_blocks = 0
-        for f, gop, (n, h, w, bh, bw, s0, m0, k0) in zip(sets, gops, geo):
-            max_blocks = max(max_blocks, bh * bw)
-            for fi in range(n):
-                for p in range(3):
-                    k = k0 + 3 * fi + p
-                    q = rp[k]
-                    q.cur = f[fi, p].data_ptr()
-                    q.prev = f[fi - 1, p].data_ptr() if fi % gop else None
-                    q.pitch = f.stride(2)
-                    q.symbols = symbols.data_ptr() + s0 + (3 * fi + p) * h * w
-                    q.modes = modes.data_ptr() + m0 + (3 * fi + p) * bh * bw
-                    q.height, q.width = h, w
-                    e = rc[k]
-                    e.payload = payload.data_ptr() + int(cap_off[k])
-                    e.symbols = q.symbols
-                    e.n_symbols = h * w
-        d_rp = _to_device_struct_array(rp, dev)
-        d_rc = _to_device_struct_array(rc, dev)
+        rc["payload"][:n_planes] = payload.data_ptr() + cap_off[:-1]
         sp = _dev.stream_ptr(s)
-        _lib.call("kvf_kvfc_residuals", _dev.ptr(d_rp), n_planes, max_blocks, sp)
-        _lib.call("kvf_rc_encode", _dev.ptr(d_rc), n_planes, _dev.ptr(out_len), sp)
-        lens = out_len.cpu().numpy()
+        _lib.call("kvf_kvfc_residuals", _dev.ptr(_to_dev_struct(rp, dev)), n_planes, max_blocks, sp)
+        _lib.call("kvf_rc_encode", _dev.ptr(_to_dev_struct(rc, dev)), n_planes, _dev.ptr(out_len), sp)
+        lens = out_len.cpu().numpy()[:n_planes]
         modes_h = modes.cpu().numpy()
-        # stream layout (fk/codec.py:16-20) and the pieces to gather
-        results, pieces, total = [], [], 0
-        layouts = []
-        for gop, (n, h, w, bh, bw, s0, m0, k0) in zip(gops, geo):
+        # stream layout (fk/codec.py:16-20): header | per frame: type, per plane:
+        # [inter: packed modes] u32 len, payload — positions by cumulative sums
+        layouts, piece_parts, total = [], [], 0
+        for gop, (n, h, w, bh, bw, hw4, s0, m0, k0) in zip(gops, geo):
             blen = (bh * bw + 7) // 8
-            pos = 12
-            frame_offsets, inter_frac, fields = [], [], []
-            for fi in range(n):
-                frame_offsets.append(pos)
-                is_inter = fi % gop != 0
-                fields.append((pos, 1 if is_inter else 0, None))
-                pos += 1
-                fracs = []
-                for p in range(3):
-                    k = k0 + 3 * fi + p
-                    if is_inter:
-                        mo = m0 + (3 * fi + p) * bh * bw
-                        pieces.append((modes.data_ptr() + mo, total + pos, bh * bw, 1))
-                        fracs.append(float(modes_h[mo:mo + bh * bw].mean()))
-                        pos += blen
-                    fields.append((pos, None, int(lens[k])))
-                    pos += 4
-                    pieces.append((payload.data_ptr() + int(cap_off[k]), total + pos, int(lens[k]), 0))
-                    pos += int(lens[k])
-                inter_frac.append(float(np.mean(fracs)) if fracs else 0.0)
-            layouts.append((total, pos, n, h, w, frame_offsets, inter_frac, fields))
-            total += pos
+            k = np.arange(3 * n, dtype=np.int64)
+            fi, p = k // 3, k % 3
+            inter = (fi % gop) != 0
+            ln = lens[k0:k0 + 3 * n]
+            plane_bytes = np.where(inter, blen, 0) + 4 + ln          # per (frame, plane)
+            frame_bytes = 1 + plane_bytes.reshape(n, 3).sum(axis=1) if n else np.zeros(0, np.int64)
+            frame_off = 12 + np.concatenate([[0], np.cumsum(frame_bytes)[:-1]]).astype(np.int64)
+            within = np.concatenate([np.zeros((n, 1), np.int64),
+                                     np.cumsum(plane_bytes.reshape(n, 3), axis=1)[:, :2]],
+                                    axis=1).reshape(-1) if n else np.zeros(0, np.int64)
+            plane_off = frame_off[fi] + 1 + within                    # start of plane field
+            len_off = plane_off + np.where(inter, blen, 0)           # u32 length field
+            size = int(12 + frame_bytes.sum())
+            # gather pieces: payloads, and mode bitmaps of inter planes (packbits)
+            pay = np.zeros(3 * n, _PIECE_DTYPE)
+            pay["src"] = payload.data_ptr() + cap_off[k0:k0 + 3 * n]
+            pay["dst_off"] = total + len_off + 4
+            pay["len"] = ln
+            bm = np.zeros(int(inter.sum()), _PIECE_DTYPE)
+            bm["src"] = modes.data_ptr() + m0 + k[inter] * bh * bw
+            bm["dst_off"] = total + plane_off[inter]
+            bm["len"] = bh * bw
+            bm["pack_bits"] = 1
+            piece_parts += [pay, bm]
+            mv = modes_h[m0:m0 + 3 * n * bh * bw].reshape(n, 3, bh * bw) if n else None
+            inter_frac = ([0.0 if f % gop == 0 else float(mv[f].mean()) for f in range(n)]
+                          if n else [])
+            layouts.append((total, size, n, h, w, frame_off, inter, len_off, ln, inter_frac))
+            total += size
         blob = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
-        pc = (_lib.kvf_piece * max(1, len(pieces)))()
-        for j, (src, off, ln, pb) in enumerate(pieces):
-            pc[j].src, pc[j].dst_off, pc[j].len, pc[j].pack_bits = src, off, ln, pb
-        d_pc = _to_device_struct_array(pc, dev)
-        _lib.call("kvf_gather", _dev.ptr(d_pc), len(pieces), _dev.ptr(blob), sp)
+        pieces = np.concatenate(piece_parts) if piece_parts else np.zeros(1, _PIECE_DTYPE)
+        _lib.call("kvf_gather", _dev.ptr(_to_dev_struct(pieces, dev)), len(pieces) if piece_parts else 0,
+                  _dev.ptr(blob), sp)
         host = blob.cpu().numpy()
-    for (base, size, n, h, w, frame_offsets, inter_frac, fields) in layouts:
-        buf = bytearray(host[base:base + size].tobytes())
-        struct.pack_into("<III", buf, 0, n, h, w)
-        for pos, ftype, plen in fields:
-            if ftype is not None:
-                buf[pos] = ftype
-            else:
-                struct.pack_into("<I", buf, pos, plen)
-        results.append(Bitstream(bytes(buf), n, h, w, frame_offsets, inter_frac))
+    results = []
+    for (base, size, n, h, w, frame_off, inter, len_off, ln, inter_frac) in layouts:
+        buf = host[base:base + size]      # header fields written in place, one copy out
+        buf[:12] = np.array([n, h, w], "<u4").view(np.uint8)
+        buf[frame_off] = inter.reshape(n, 3)[:, 0].astype(np.uint8) if n else buf[frame_off]
+        lb = ln.astype("<u4").view(np.uint8).reshape(-1, 4)
+        for b in range(4):
+            buf[len_off + b] = lb[:, b]
+        results.append(Bitstream(buf.tobytes(), n, h, w, [int(x) for x in frame_off], inter_frac))
     return results
 
 

@@ -10,15 +10,15 @@
 //    stream buffer at host-computed offsets (fk/codec.py:16-20 layout).
 #include <algorithm>
 
-#include "kvf_common.cuh"
+#include "kvf_rc_model.cuh"
 
 namespace kvf {
 namespace {
 
-constexpr uint32_t kTop = 1u << 24;
-constexpr uint32_t kBot = 1u << 16;
-constexpr uint32_t kInc = 32;
-constexpr uint32_t kLimit = 1u << 16;
+using rc::kBot;
+using rc::kInc;
+using rc::kLimit;
+using rc::kTop;
 
 __device__ __forceinline__ uint32_t zig(int r) {
   const int s = (int)(int8_t)(uint8_t)(r & 0xFF);  // residual mod 256 as signed byte
@@ -60,62 +60,103 @@ __global__ void resid_kernel(const kvf_resid_plane* __restrict__ planes) {
     }
 }
 
-__global__ void __launch_bounds__(224)
+// The encoder runs the decoder's model (kvf_rc_model.cuh): a symbol's cum and
+// count come straight from its block (two u16 reads), the division is the exact
+// fp32 one, the "top byte settled" output phase is clz(low ^ (low + rng)) / 8
+// bytes at once, and output bytes collect in a 64-bit accumulator so a 4-byte
+// aligned stream is written a word at a time.
+__global__ void __launch_bounds__(rc::kDecThreads)
     rc_encode_kernel(const kvf_rc_stream* __restrict__ streams, int n, int64_t* out_len) {
-  extern __shared__ uint32_t W[];  // [256][blockDim.x], W[i] = fen[i+1] << 16 | freq[i]
-  const int nt = blockDim.x, tid = threadIdx.x;
-  const int sidx = blockIdx.x * nt + tid;
+  using namespace rc;
+  extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B, as the decoder's
+  const int tid = threadIdx.x;
+  const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
   const kvf_rc_stream st = streams[sidx];
-#define MW(i) W[(i) * nt + tid]
-  for (int i = 0; i < 256; ++i) {
-    const int j = i + 1;
-    MW(i) = ((uint32_t)(j & -j) << 16) | 1u;
-  }
+  uint4* m = M + tid;
+  uint32_t CB[16];
+  model_init(m, CB);
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu;
   uint8_t* out = const_cast<uint8_t*>(st.payload);
-  int64_t n_out = 0;
+  const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  uint64_t acc = 0;    // pending output bytes, first byte lowest
+  uint32_t pend = 0;   // number of pending bytes (< 4 between symbols)
+  int64_t n_out = 0;   // bytes written to `out`
+  auto emit = [&](uint32_t v, uint32_t nb) {  // v: nb bytes, first in the low byte
+    acc |= (uint64_t)v << (8 * pend);
+    pend += nb;
+    if (pend >= 4) {
+      if (aligned4) {
+        *reinterpret_cast<uint32_t*>(out + n_out) = (uint32_t)acc;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[n_out + e] = (uint8_t)(acc >> (8 * e));
+      }
+      n_out += 4;
+      acc >>= 32;
+      pend -= 4;
+    }
+  };
   const uint8_t* sym = st.symbols;
-  for (int64_t k = 0; k < st.n_symbols; ++k) {
+  const uint32_t nsym = (uint32_t)st.n_symbols;
+  float rcp = rcp_approx(total);
+  for (uint32_t k = 0; k < nsym; ++k) {
     const uint32_t s = __ldg(sym + k);
-    uint32_t cum = 0;  // Fenwick prefix sum of freq[0..s-1]
-    for (uint32_t j = s; j > 0; j -= j & (0u - j)) cum += MW(j - 1) >> 16;
-    const uint32_t fr = MW(s) & 0xFFFFu;
-    const uint32_t r = rng / total;
+    const float rcp_next = rcp_approx(total + kInc);
+    const uint32_t blk = s >> 4, sl = s & 15;
+    const uint4 ca = m[(2 * blk) * kDecThreads], cb = m[(2 * blk + 1) * kDecThreads];
+    const uint32_t wv[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+    // incl[sl] and incl[sl - 1] (0 at sl = 0): two direct u16 loads
+    const uint16_t* m16 = reinterpret_cast<const uint16_t*>(m);
+    const uint32_t hi_v = m16[((2 * blk + (sl >> 3)) * kDecThreads) * 8 + (sl & 7)];
+    const uint32_t j1 = sl - 1;  // wraps for sl == 0 (value unused then)
+    const uint32_t lo_raw = m16[((2 * blk + ((j1 >> 3) & 1)) * kDecThreads) * 8 + (j1 & 7)];
+    const uint32_t lo_v = sl == 0 ? 0u : lo_raw;
+    // CB[blk] by a 4-level select tree on the bits of blk
+    uint32_t base;
+    {
+      const bool k3 = blk & 8, k2 = blk & 4, k1 = blk & 2, k0 = blk & 1;
+      uint32_t e[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) e[i] = k3 ? CB[8 + i] : CB[i];
+      uint32_t f4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) f4[i] = k2 ? e[4 + i] : e[i];
+      const uint32_t g0 = k1 ? f4[2] : f4[0], g1 = k1 ? f4[3] : f4[1];
+      base = k0 ? g1 : g0;
+    }
+    const uint32_t cum = base + lo_v, fr = hi_v - lo_v;     // fk/rangecoder.py:114-115
+    const uint32_t r = exact_div(rng, total, rcp);          // fk/rangecoder.py:117
     low += r * cum;
     rng = r * fr;
-    for (;;) {
-      if ((low ^ (low + rng)) >= kTop) {
-        if (rng >= kBot) break;
-        rng = (0u - low) & (kBot - 1);
+    {  // fk/rangecoder.py:120-131: settled top bytes, then (rarely) squeezes
+      const uint32_t nb = __clz(low ^ (low + rng)) >> 3;
+      if (nb) {
+        emit(__byte_perm(low, 0u, 0x0123) & ((1u << (8 * nb)) - 1u), nb);
+        low <<= 8 * nb;
+        rng <<= 8 * nb;
       }
-      out[n_out++] = (uint8_t)(low >> 24);
-      low <<= 8;
-      rng <<= 8;
+      while (rng < kBot || (low ^ (low + rng)) < kTop) {
+        if ((low ^ (low + rng)) >= kTop) rng = (0u - low) & (kBot - 1);
+        emit(low >> 24, 1);
+        low <<= 8;
+        rng <<= 8;
+      }
     }
-    MW(s) += (kInc << 16) | kInc;
-    for (uint32_t j = (s + 1) + ((s + 1) & (0u - (s + 1))); j <= 255; j += j & (0u - j))
-      MW(j - 1) += kInc << 16;
+    model_update(m, CB, blk, sl, wv);                       // fk/rangecoder.py:133-135
     total += kInc;
-    if (total >= kLimit) {
-      total = 0;
-      for (int i = 0; i < 256; ++i) {
-        const uint32_t f = ((MW(i) & 0xFFFFu) + 1) >> 1;
-        total += f;
-        MW(i) = (f << 16) | f;
-      }
-      for (int j = 1; j <= 255; ++j) {
-        const int par = j + (j & -j);
-        if (par <= 255) MW(par - 1) += MW(j - 1) & 0xFFFF0000u;
-      }
+    rcp = rcp_next;
+    if (total >= kLimit) {                                  // fk/rangecoder.py:136-137
+      total = rebuild(m, CB);
+      rcp = rcp_approx(total);
     }
   }
   for (int k = 0; k < 4; ++k) {  // flush: four bytes pin down the final interval
-    out[n_out++] = (uint8_t)(low >> 24);
+    emit(low >> 24, 1);
     low <<= 8;
   }
-  out_len[sidx] = n_out;
-#undef MW
+  for (uint32_t e = 0; e < pend; ++e) out[n_out + e] = (uint8_t)(acc >> (8 * e));
+  out_len[sidx] = n_out + pend;
 }
 
 __global__ void gather_kernel(const kvf_piece* __restrict__ pieces, uint8_t* dst) {
@@ -157,16 +198,10 @@ extern "C" kvf_status kvf_rc_encode(const kvf_rc_stream* d_streams, int32_t n_st
   if (n_streams < 0 || (n_streams > 0 && (!d_streams || !d_out_len)))
     KVF_FAIL(KVF_EINVAL, "bad stream array");
   if (n_streams == 0) return KVF_OK;
-  int dev = 0, sms = 0;
-  KVF_CHECK_CUDA(cudaGetDevice(&dev));
-  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int per = (n_streams + sms - 1) / sms;
-  per = std::min(224, std::max(32, (per + 31) / 32 * 32));
-  const size_t smem = (size_t)per * 256 * sizeof(uint32_t);
-  KVF_CHECK_CUDA(cudaFuncSetAttribute(rc_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(224 * 256 * sizeof(uint32_t))));
-  const int grid = (n_streams + per - 1) / per;
-  rc_encode_kernel<<<grid, per, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+  // one warp per CTA, 16 KB of models (the decoder's layout)
+  const size_t smem = (size_t)rc::kDecThreads * 256 * sizeof(uint16_t);
+  const int grid = (n_streams + rc::kDecThreads - 1) / rc::kDecThreads;
+  rc_encode_kernel<<<grid, rc::kDecThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       d_streams, n_streams, d_out_len);
   KVF_CHECK_CUDA(cudaGetLastError());
   return KVF_OK;
