@@ -151,11 +151,6 @@ class _PinnedStaging:
 _STAGING = _PinnedStaging()
 
 
-def _to_device_struct_array(arr, device) -> torch.Tensor:
-    raw = np.frombuffer(bytes(arr), np.uint8) if C.sizeof(arr) else np.zeros(1, np.uint8)
-    return torch.from_numpy(raw.copy()).to(device)
-
-
 def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     """Decode many KVFC streams on the GPU in one pair of launches.
 

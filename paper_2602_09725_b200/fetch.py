@@ -211,7 +211,7 @@ def _mem_for(mem, cache_id):
 
 def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=None,
                         initial_active="R1080", timeout_s=30.0, on_chunk=None, *, mem=None,
-                        scales_dtype_out=None, real_layers=None, depth=32, max_batch=32,
+                        real_layers=None, depth=32, max_batch=32,
                         fetch_fn=None, workers=1):
     """Fetch chunks from a live server and decode them on the GPU as they arrive.
 

@@ -383,3 +383,38 @@ def test_baseline_config_units_match_oracle(shape):
                 assert got is None                               # pad layer never written
             else:
                 assert torch.equal(got.cpu(), deq[t, p].reshape(-1)), (name, t, p)
+
+
+@pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
+                                 (8, 128, 2, 4, 16, 8), (4, 64, 1, 4, 64, 1)])
+def test_apply_inverse_layout_match_oracle(lay):
+    """apply_layout / inverse_layout (fk/layout.py:123-147) on one token's 3 layers."""
+    H, D = lay[0], lay[1]
+    cfg = L.LayoutConfig(*lay)
+    v = np.random.default_rng(3).integers(-127, 128, size=(3, H * D)).astype(np.int8)
+    tile = L.apply_layout(torch.from_numpy(v)[None], cfg)
+    oplan = ref.Plan(1, "R240", *lay, F=4)
+    assert np.array_equal(tile.cpu().numpy(), oplan.tile(v))
+    back = L.inverse_layout(tile, cfg)
+    assert np.array_equal(back.reshape(3, H * D).cpu().numpy(), v)
+
+
+def test_paged_memory_accounting_like_reference():
+    """PagedMemory byte accounting, write-once conflicts, begin_fetch and
+    free_page (fk/kvmodel.py:195-244; tests/test_kvmodel.py:145-179)."""
+    mem = KV.PagedMemory(page_size_tokens=4, dtype=torch.int8)
+    slot = torch.arange(16, dtype=torch.int8)
+    for t in range(6):
+        mem.page_write(t, 0, slot)
+    assert mem.allocated_bytes == 6 * 16 and mem.peak_bytes == 6 * 16
+    with pytest.raises(KV.ConflictError):
+        mem.page_write(2, 0, slot)
+    mem.begin_fetch()                          # markers cleared, contents kept
+    mem.page_write(2, 0, slot + 1)
+    assert torch.equal(mem.read(2, 0).cpu(), slot + 1)
+    assert mem.allocated_bytes == 7 * 16       # re-written slot counted again
+    mem.free_page(0)                           # tokens 0..3 leave the cache
+    assert mem.read(1, 0) is None and torch.equal(mem.read(4, 0).cpu(), slot)
+    assert mem.allocated_bytes == 3 * 16 and mem.peak_bytes == 7 * 16   # as the reference counts
+    mem.page_write(1, 0, slot)                 # the freed page can be written again
+    assert torch.equal(mem.read(1, 0).cpu(), slot)
