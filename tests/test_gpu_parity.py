@@ -418,3 +418,31 @@ def test_paged_memory_accounting_like_reference():
     assert mem.allocated_bytes == 3 * 16 and mem.peak_bytes == 7 * 16   # as the reference counts
     mem.page_write(1, 0, slot)                 # the freed page can be written again
     assert torch.equal(mem.read(1, 0).cpu(), slot)
+
+
+@pytest.mark.parametrize("H,D,gs", [(64, 128, 128), (32, 64, 64), (1, 128, 32)])
+def test_wide_and_narrow_caches_pack_restore(H, D, gs):
+    """Channel widths outside the vectorised kernels (C = 8192: generic path) and
+    a single-head cache with 32-channel groups: pack and restore vs the oracle."""
+    T, res = 37, "R240"
+    lay = (H, D, 1, H, 1, D)
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, 3, H, D, 0.9, 2, 0.3))
+    kv = np_bf16_from_f32(x).cuda()
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+    fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
+    am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)), dtype=torch.int32,
+                     device="cuda")
+    sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
+    u, _ = _pack_unit(kv, lay, res, 0, T, 4, gs, fr, am, sc)
+    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
+    torch.cuda.synchronize()
+    v, s = ref.quantize(x, gs)
+    want = ref.assemble_frames(v.reshape(T, 3, H * D), ref.Plan(T, res, *lay, F=4))
+    np.testing.assert_array_equal(sc.cpu().numpy(), s)
+    np.testing.assert_array_equal(fr.cpu().numpy(), want)
+    mem = KV.PagedMemory(16, dtype=torch.bfloat16)
+    restore_frames(fr, plan, mem, 0, 0, scales=sc)
+    deq = torch.from_numpy(ref.dequantize(v, s, gs)).to(torch.bfloat16)
+    for t in (0, 17, T - 1):
+        for p in range(3):
+            assert torch.equal(mem.read(t, p).cpu(), deq[t, p].reshape(-1))
