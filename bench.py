@@ -191,7 +191,7 @@ class Workload:
         self.all_units = len(all_units)
         self.mine = shard.units_for_rank(all_units, rank, world, args.shard, H, D)
         self.pack_units, self.units, self.frames, self.scales = [], [], [], []
-        self.caches, self._keep = [], []
+        self.caches, self._keep, self._specs = [], [], []
         self.elems = sum(u.elements(H, D) for u in self.mine)
         keys = sorted({(u.request, u.kv, u.triplet) for u in self.mine})
         for (r, kv_i, j) in keys:
@@ -227,6 +227,7 @@ class Workload:
                 dst.slot_stride = H * D
                 dst.head_stride = D
                 dst.token_base = t0
+                self._specs.append((src, dst, tc))
                 pu = _lib.kvf_pack_unit()
                 pu.src = src
                 pu.plan = plan.to_c(self.gs)
@@ -241,9 +242,32 @@ class Workload:
         self.frame_bytes = sum(f.numel() for f in self.frames)
         self._pack_arr = (_lib.kvf_pack_unit * len(self.pack_units))(*self.pack_units)
         self._restore_arr = (_lib.kvf_restore_unit * len(self.units))(*self.units)
-        self._lib, self._dev = _lib, _dev
+        self._lib, self._dev, self._L = _lib, _dev, L
         self.n_launch_restore = (len(self.units) + _lib.KVF_MAX_UNITS - 1) // _lib.KVF_MAX_UNITS
         self.n_launch_pack = 4 * self.n_launch_restore
+
+    def frames_at(self, res):
+        """Pack every unit again at another resolution class (same sources,
+        caches and scales); returns (frames, restore unit descriptors)."""
+        torch = self.torch
+        from paper_2602_09725_b200.restore import make_restore_unit
+        frames, pus, rus, keep = [], [], [], []
+        for (src, dst, tc), sc in zip(self._specs, self.scales):
+            plan = self._L.plan_inter_frame(tc, res, self.lay, 4)
+            fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device=sc.device)
+            am = torch.zeros(self._lib.load().kvf_pack_scratch_words(plan.to_c(self.gs)),
+                             dtype=torch.int32, device=sc.device)
+            pu = self._lib.kvf_pack_unit()
+            pu.src, pu.plan, pu.absmax, pu.scales = src, plan.to_c(self.gs), am.data_ptr(), sc.data_ptr()
+            pu.frames = self._dev.surface_of(fr)
+            pus.append(pu)
+            rus.append(make_restore_unit(fr, plan, sc, dst, self.gs))
+            frames.append(fr)
+            keep.append(am)
+        arr = (self._lib.kvf_pack_unit * len(pus))(*pus)
+        self._lib.call("kvf_pack_batch", arr, len(pus), self._dev.stream_ptr(torch.cuda.current_stream()))
+        torch.cuda.synchronize()
+        return frames, rus
 
     def pack(self, stream):
         self._lib.call("kvf_pack_batch", self._pack_arr, len(self.pack_units),
@@ -335,24 +359,26 @@ def e2e_restore(w, steps, torch):
     return ms, w.frame_bytes, out_host.numel() * 2
 
 
-def fetch_to_ready(w, steps, torch):
+def fetch_to_ready(w, steps, torch, frames_units=None):
     """Fetch-to-ready of the whole context from coded KVFC streams in pinned host
     memory (what a fetch receives): per step one H2D of every stream's bytes,
     GPU entropy decode + reconstruction of all 88 units (codec.decode_batch: 2
     launches), then the batched restore into the paged cache.  Wall clock,
     host work included; the network leg is modelled from the coded bytes."""
     from paper_2602_09725_b200 import _lib, codec
+    src_frames, src_units = frames_units if frames_units else (w.frames, w.units)
+    frame_bytes = sum(f.numel() for f in src_frames)
     t0 = time.perf_counter()
-    streams = [bs.data for bs in codec.encode_batch(w.frames, [4] * len(w.frames))]
+    streams = [bs.data for bs in codec.encode_batch(src_frames, [4] * len(src_frames))]
     enc_s = time.perf_counter() - t0
     coded = sum(len(b) for b in streams)
     # what a fetch's receive ring holds: the coded bytes in pinned host memory
     streams = [torch.frombuffer(bytearray(b), dtype=torch.uint8).pin_memory() for b in streams]
     indices = [codec.StreamIndex(b) for b in streams]
     frames, _ = codec.decode_batch(streams, indices=indices)
-    ok = all(torch.equal(a, b) for a, b in zip(frames, w.frames))
+    ok = all(torch.equal(a, b) for a, b in zip(frames, src_frames))
     units = []
-    for u, fr in zip(w.units, frames):
+    for u, fr in zip(src_units, frames):
         nu = _lib.kvf_restore_unit()
         ctypes_copy(nu, u)
         nu.frames.base = fr.data_ptr()
@@ -376,8 +402,8 @@ def fetch_to_ready(w, steps, torch):
         scan.append((t2 - t1) * 1e3)
     ms = statistics.median(times)
     return {"ms": round(ms, 2), "scan_ms": round(statistics.median(scan), 2),
-            "coded_bytes": coded, "frame_bytes": w.frame_bytes,
-            "ratio_int8_over_coded": round(w.frame_bytes / coded, 3),
+            "coded_bytes": coded, "frame_bytes": frame_bytes,
+            "ratio_int8_over_coded": round(frame_bytes / coded, 3),
             "decode_bitexact": ok, "encode_s": round(enc_s, 2),
             "link_s": {f"{g}gbps": round(coded * 8 / (g * 1e9), 3) for g in (10, 25, 100)}}
 
@@ -509,6 +535,10 @@ def main():
     fetch = None
     if not args.no_fetch:
         fetch = fetch_to_ready(w, 3, torch)
+        fetch["resolution"] = args.res
+        if args.res != "R240":  # the class the adaptive policy picks at >= 10 Gbps
+            alt = fetch_to_ready(w, 3, torch, w.frames_at("R240"))
+            fetch["R240"] = {k: alt[k] for k in ("ms", "coded_bytes", "decode_bitexact")}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
