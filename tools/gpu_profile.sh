@@ -10,7 +10,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch_stdout.txt 2>&1
 echo "launch list rc=$?"
 FULL="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e ${BENCH_ARGS}"
-for k in ${KERNELS:-restore_fast absmax_fast pack_fast rc_decode recon_kernel}; do
+for k in ${KERNELS:-restore_fast absmax_fast pack_fast rc_decode recon_kernel rc_encode}; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o gpurun_out/prof_$k -f $FULL > gpurun_out/ncu_${k}_stdout.txt 2>&1
   echo "$k rc=$?"
