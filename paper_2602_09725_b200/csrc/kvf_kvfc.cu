@@ -8,8 +8,9 @@
 //    prefix sums in registers, within-block prefix sums as packed u16 in
 //    shared memory — 512 B per stream), both searches are 4-level binary
 //    searches over registers, the second division is replaced by multiplies,
-//    renormalisation is three predicated rounds over a prefetched 64-bit byte
-//    window, and a symbol's model update is two 128-bit stores.
+//    renormalisation is closed-form (clz of low ^ (low + rng)) over a
+//    prefetched 64-bit byte window, and a symbol's model update is two 128-bit
+//    stores.
 // 2. recon_kernel: per-sample prediction (fk/codec.py:131-144) as segmented
 //    prefix sums mod 256.  One CTA per chain of same-plane frames starting at
 //    an intra frame.  A 16-pixel run of a row never crosses a 16x16 block, so a

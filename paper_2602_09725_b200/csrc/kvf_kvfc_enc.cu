@@ -4,8 +4,8 @@
 //    inter residual SADs, mode = inter iff SAD_inter <= SAD_intra, then the
 //    zigzag symbols of the chosen residual (fk/codec.py:77-123).
 // 2. rc_encode_kernel: the reference's adaptive range encoder
-//    (fk/rangecoder.py:106-143), one thread per (frame, plane) stream, with the
-//    same packed Fenwick model in shared memory as the decoder (kvf_kvfc.cu).
+//    (fk/rangecoder.py:106-143), one thread per (frame, plane) stream, on the
+//    decoder's cumulative-count model (kvf_rc_model.cuh).
 // 3. gather_kernel: scatters payloads and packed mode bitmaps into the final
 //    stream buffer at host-computed offsets (fk/codec.py:16-20 layout).
 #include <algorithm>

@@ -1,4 +1,4 @@
-// kvf_pack_common.cuh — pieces shared by the phase-split and fused pack kernels:
+// kvf_pack_common.cuh — pieces shared by the phase-split and team pack kernels:
 // unit descriptor, source vector loads, |x| maxima, and the exact quantiser.
 //
 // Quantisation is the reference's (fk/kvmodel.py:127-144): per (layer, group)
