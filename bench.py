@@ -374,7 +374,7 @@ def fetch_to_ready(w, steps, torch, frames_units=None):
     coded = sum(len(b) for b in streams)
     # what a fetch's receive ring holds: the coded bytes in pinned host memory
     streams = [torch.frombuffer(bytearray(b), dtype=torch.uint8).pin_memory() for b in streams]
-    indices = [codec.StreamIndex(b) for b in streams]
+    indices = codec.index_streams(streams)
     frames, _ = codec.decode_batch(streams, indices=indices)
     ok = all(torch.equal(a, b) for a, b in zip(frames, src_frames))
     units = []
@@ -395,7 +395,7 @@ def fetch_to_ready(w, steps, torch, frames_units=None):
     times, scan = [], []
     for _ in range(steps):
         t1 = time.perf_counter()
-        idx = [codec.StreamIndex(b) for b in streams]   # host stream walk, per fetch
+        idx = codec.index_streams(streams)   # host stream walk, per fetch
         t2 = time.perf_counter()
         step(idx)
         times.append((time.perf_counter() - t1) * 1e3)

@@ -221,7 +221,9 @@ typedef struct kvf_kvfc_info {
  * For frame f, plane p (k = 3f + p): payload_off[k], payload_len[k] (the u32
  * length prefix), bitmap_off[k] (-1 for intra frames); frame_type[f].
  * Arrays hold cap_frames frames (3*cap_frames entries); with cap_frames <
- * n_frames only `info` is filled and KVF_EINVAL is returned.  Returns
+ * n_frames only the header is read, `info` is filled and KVF_EINVAL is
+ * returned (a size query: the walk and its checks run on the fill call;
+ * header errors are reported by both).  Returns
  * KVF_EDECODE and *bad_frame on every condition where the reference raises
  * DecodeError (short header, truncated type/bitmap/length/payload, bad frame
  * type, inter frame without reference, trailing bytes). */

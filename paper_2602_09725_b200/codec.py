@@ -121,6 +121,32 @@ class StreamIndex:
         _lib.check(st)
 
 
+_SCAN_POOL = None
+_SCAN_POOL_LOCK = threading.Lock()
+
+
+def index_streams(datas) -> list:
+    """StreamIndex of every stream, walked in parallel on host threads.
+
+    The walk is a pointer chase through the stream (each plane's length word
+    gives the next position), one cache/TLB miss per plane, and kvf_kvfc_scan
+    runs without the GIL, so streams are spread over a small thread pool.
+    Errors are raised as by StreamIndex, for the first failing stream in order.
+    """
+    global _SCAN_POOL
+    datas = list(datas)
+    if len(datas) < 4:
+        return [StreamIndex(d) for d in datas]
+    with _SCAN_POOL_LOCK:
+        if _SCAN_POOL is None:
+            import concurrent.futures
+            import os
+            _SCAN_POOL = concurrent.futures.ThreadPoolExecutor(
+                max_workers=max(1, min(8, (os.cpu_count() or 2) // 2)),
+                thread_name_prefix="kvfc-scan")
+    return list(_SCAN_POOL.map(StreamIndex, datas))
+
+
 class _PinnedStaging:
     """Grow-only pinned host buffer for the coded bytes of a decode batch.
 
@@ -166,7 +192,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     dev = _dev.device()
     pinned_in = all(isinstance(x, torch.Tensor) for x in streams) and len(streams) > 0
     datas = list(streams) if pinned_in else [_as_bytes(x) for x in streams]
-    idxs = indices if indices is not None else [StreamIndex(d) for d in datas]
+    idxs = indices if indices is not None else index_streams(datas)
     if ranges is None:
         ranges = [(0, ix.n) for ix in idxs]
     for ix, (f0, f1) in zip(idxs, ranges):
@@ -187,91 +213,188 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     sizes = [hi - lo for lo, hi in spans]
     starts = np.cumsum([0] + sizes)
     s = stream if stream is not None else torch.cuda.current_stream()
-    if pinned_in:  # receive buffers already in (pinned) host memory: H2D each span
-        with torch.cuda.stream(s):
-            blob = torch.empty(int(starts[-1]) or 1, dtype=torch.uint8, device=dev)
-            for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
-                if hi > lo:
-                    blob[s0:s0 + hi - lo].copy_(d[lo:hi], non_blocking=True)
-    else:
+    live = [j for j, (f0, f1) in enumerate(ranges) if f1 > f0]
+    parts = _split_parts(live, [sizes[j] for j in live])
+    host = None
+    if not pinned_in:
         host = _STAGING.acquire(int(starts[-1]) or 1)
         hv = host.numpy()
         for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
             hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
-        with torch.cuda.stream(s):
-            blob = host.to(dev, non_blocking=True)
-            _STAGING.release(s)
-    # shift so that stream offsets index the copied span
-    starts = starts - np.array([lo for lo, _ in spans] + [0])
+    hw_all = np.array([ix.h * ix.w for ix in idxs], np.int64)
+    hw16_all = -(-hw_all // 16) * 16                 # 16-byte aligned symbol slots
+    nf_all = np.array([f1 - f0 for f0, f1 in ranges], np.int64)
+    sym_at = np.concatenate([[0], np.cumsum(3 * nf_all * hw16_all)])
+    frames = []
     with torch.cuda.stream(s):
-        frames = []
-        n_fr = [f1 - f0 for f0, f1 in ranges]
-        n_sym = sum(3 * nf * (-(-ix.h * ix.w // 4) * 4) for nf, ix in zip(n_fr, idxs))
-        symbols = torch.empty(max(n_sym, 1), dtype=torch.uint8, device=dev)
-        base = blob.data_ptr()
-        sym_base = symbols.data_ptr()
-        rc_parts, plane_parts, chain_parts = [], [], []
-        sym_at = 0
-        n_planes = 0
+        blob = torch.empty(int(starts[-1]) or 1, dtype=torch.uint8, device=dev)
+        symbols = torch.empty(max(int(sym_at[-1]), 1), dtype=torch.uint8, device=dev)
         for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
-            nf = f1 - f0
-            fr = out[j] if out is not None else torch.empty((nf, 3, ix.h, ix.w),
+            fr = out[j] if out is not None else torch.empty((f1 - f0, 3, ix.h, ix.w),
                                                            dtype=torch.uint8, device=dev)
-            if tuple(fr.shape) != (nf, 3, ix.h, ix.w):
+            if tuple(fr.shape) != (f1 - f0, 3, ix.h, ix.w):
                 raise ValueError("output frames have the wrong shape")
             frames.append(fr)
-            if nf == 0:
-                continue
-            hw = ix.h * ix.w
-            hw4 = -(-hw // 4) * 4                          # 4-byte aligned symbol slots
-            ks = np.arange(3 * f0, 3 * f1)                 # stream k = 3 f + p, frame-major
-            loc = ks - 3 * f0
-            stream_base = base + int(starts[j])
-            rc = np.empty(len(ks), _RC_DTYPE)
-            rc["payload"] = stream_base + ix.payload_off[ks]
-            rc["len"] = ix.payload_len[ks]
-            rc["symbols"] = sym_base + sym_at + loc * hw4
-            rc["n_symbols"] = hw
-            pl = np.empty(len(ks), _PLANE_DTYPE)
-            pl["symbols"] = rc["symbols"]
-            pl["modes"] = np.where(ix.bitmap_off[ks] >= 0, stream_base + ix.bitmap_off[ks], 0)
-            pl["out"] = fr.data_ptr() + (loc // 3) * fr.stride(0) + (loc % 3) * fr.stride(1)
-            pl["out_pitch"] = fr.stride(2)
-            rc_parts.append(rc)
-            sym_at += len(ks) * hw4
-            if hw:
-                # chains: per plane, the frames from each intra frame to the next
-                # one (a reconstruction dependency chain), contiguous in `flat`
-                f = ks // 3
-                seg = np.cumsum(ix.frame_type[f0:f1] == 0)[f - f0]
-                order = np.lexsort((f, ks % 3, seg))
-                plane_parts.append(pl[order])
-                key = seg[order] * 3 + (ks % 3)[order]
-                first = np.flatnonzero(np.r_[True, key[1:] != key[:-1]])
-                ch = np.empty(len(first), _CHAIN_DTYPE)
-                ch["first"] = n_planes + first
-                ch["count"] = np.diff(np.r_[first, len(order)])
-                ch["height"], ch["width"] = ix.h, ix.w
-                chain_parts.append(ch)
-                n_planes += len(order)
-        rc = np.concatenate(rc_parts) if rc_parts else np.zeros(1, _RC_DTYPE)
-        flat = np.concatenate(plane_parts) if plane_parts else np.zeros(1, _PLANE_DTYPE)
-        ch_arr = np.concatenate(chain_parts) if chain_parts else np.zeros(1, _CHAIN_DTYPE)
-        k_rc = sum(len(x) for x in rc_parts)
-        chains = ch_arr if chain_parts else []
-        # descriptor arrays via pinned memory: asynchronous, never a host sync
-        d_rc, d_planes, d_chains = (
-            torch.from_numpy(a.view(np.uint8)).pin_memory().to(dev, non_blocking=True)
-            for a in (rc, flat, ch_arr))
-        sp = _dev.stream_ptr(s)
-        _lib.call("kvf_rc_decode", _dev.ptr(d_rc), k_rc, sp)
-        _lib.call("kvf_kvfc_reconstruct", _dev.ptr(d_planes), _dev.ptr(d_chains), len(chains), sp)
+    # Parts are pipelined on side streams: part p's descriptors and coded
+    # bytes are queued on the copy engine, then its two kernels; part p+1's
+    # host preparation and copies overlap part p's decoding.  (Every side
+    # stream first waits for the work `s` had before this call, so the memory
+    # allocated above on `s` is free.)
+    side = _side_streams(len(parts)) if len(parts) > 1 else [s]
+    for t in side:
+        if t is not s:
+            t.wait_stream(s)
+    base = blob.data_ptr()
+    done, keep = [], []
+    for p, part in enumerate(parts):
+        t = side[p]
+        with torch.cuda.stream(t):
+            rc, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, base,
+                                                 symbols.data_ptr() + sym_at, frames)
+            d_rc, d_planes, d_chains = (
+                torch.from_numpy(np.ascontiguousarray(x if len(x) else np.zeros(1, x.dtype))
+                                 .view(np.uint8)).pin_memory().to(dev, non_blocking=True)
+                for x in (rc, flat, ch_arr))
+            for j in part:
+                lo, hi = spans[j]
+                s0 = int(starts[j])
+                src = datas[j][lo:hi] if pinned_in else host[s0:s0 + hi - lo]
+                blob[s0:s0 + hi - lo].copy_(src, non_blocking=True)
+        sp = _dev.stream_ptr(t)
+        if len(rc):
+            _lib.call("kvf_rc_decode", _dev.ptr(d_rc), len(rc), sp)
+        if len(ch_arr):
+            _lib.call("kvf_kvfc_reconstruct", _dev.ptr(d_planes), _dev.ptr(d_chains), len(ch_arr),
+                      sp)
+        keep += [d_rc, d_planes, d_chains]
+        if t is not s:
+            ev = torch.cuda.Event()
+            ev.record(t)
+            done.append((t, ev))
+    for t, ev in done:
+        s.wait_event(ev)
+    if host is not None:
+        _STAGING.release(s)   # `s` now follows every part's copies
     held = blob.numel() + symbols.numel() + sum(f.numel() for f in frames)
     # keep descriptor/scratch tensors alive until the stream reaches this point
-    frames_keepalive = (blob, symbols, d_rc, d_planes, d_chains)
+    frames_keepalive = (blob, symbols, *keep, *frames)
     for t in frames_keepalive:
         t.record_stream(s)
+        for u, _ in done:
+            t.record_stream(u)
     return frames, held
+
+
+def _part_descriptors(part, idxs, ranges, starts, spans, base, sym_ptr, frames):
+    """kvf_rc_stream / kvf_recon_plane / kvf_recon_chain arrays of the streams
+    `part` (indices into idxs), vectorised over their planes.  Plane k = 3 f +
+    p of stream j (frame-major), streams in order; `starts` are blob offsets
+    of the copied spans, `sym_ptr[j]` the device symbol slots of stream j."""
+    nl = len(part)
+    nf = np.array([ranges[j][1] - ranges[j][0] for j in part], np.int64)
+    hs = np.array([idxs[j].h for j in part], np.int64)
+    ws = np.array([idxs[j].w for j in part], np.int64)
+    hw = hs * ws
+    hw16 = -(-hw // 16) * 16
+    n_pl = 3 * nf
+    K = int(n_pl.sum())
+    sid = np.repeat(np.arange(nl), n_pl)             # ordinal in the part of each plane
+    pl_at = np.concatenate([[0], np.cumsum(n_pl)])
+    loc = np.arange(K, dtype=np.int64) - pl_at[sid]  # k - 3 f0
+
+    def cat(name):
+        return np.concatenate([getattr(idxs[j], name)[3 * ranges[j][0]:3 * ranges[j][1]]
+                               for j in part])
+
+    p_off, p_len, b_off = cat("payload_off"), cat("payload_len"), cat("bitmap_off")
+    # the copied span of stream j starts at its lowest header offset
+    sbase = base + np.array([int(starts[j]) - spans[j][0] for j in part], np.int64)
+    out_ptr = np.array([frames[j].data_ptr() for j in part], np.int64)
+    st = np.array([frames[j].stride()[:3] for j in part], np.int64).reshape(nl, 3)
+    rc = np.empty(K, _RC_DTYPE)
+    rc["payload"] = sbase[sid] + p_off
+    rc["len"] = p_len
+    rc["symbols"] = np.asarray(sym_ptr)[part][sid] + loc * hw16[sid]
+    rc["n_symbols"] = hw[sid]
+    fl, pp = loc // 3, loc % 3
+    pl = np.empty(K, _PLANE_DTYPE)
+    pl["symbols"] = rc["symbols"]
+    pl["modes"] = np.where(b_off >= 0, sbase[sid] + b_off, 0)
+    pl["out"] = out_ptr[sid] + fl * st[sid, 0] + pp * st[sid, 1]
+    pl["out_pitch"] = st[sid, 2]
+    ftype = np.concatenate([idxs[j].frame_type[ranges[j][0]:ranges[j][1]] for j in part])
+    dest, ch_first, ch_count, ch_sid = _chain_layout(ftype, nf, hw)
+    flat = np.empty(K, _PLANE_DTYPE)
+    flat[dest] = pl
+    ch_arr = np.empty(len(ch_first), _CHAIN_DTYPE)
+    ch_arr["first"], ch_arr["count"] = ch_first, ch_count
+    ch_arr["height"], ch_arr["width"] = hs[ch_sid], ws[ch_sid]
+    return rc, flat, ch_arr
+
+
+def _chain_layout(ftype, nf, hw):
+    """Reconstruction order of the planes of concatenated frame ranges.
+
+    ``ftype``: frame types of every decoded frame, stream after stream (each
+    range starts with an intra frame); ``nf``: frames per stream; ``hw``:
+    samples per plane per stream.  Planes are numbered frame-major (k = 3 f +
+    p over the concatenated frames).  A chain is one plane index over a
+    segment (an intra frame and the inter frames after it), in frame order:
+    segment g of n frames starting at global frame a owns slots [3a, 3a + 3n),
+    plane index p's chain at 3a + p n.  Returns (dest slot of each plane,
+    chain first slots, chain lengths, stream ordinal of each chain); chains of
+    empty planes (hw == 0) are dropped.
+    """
+    ftype = np.asarray(ftype)
+    nf = np.asarray(nf, np.int64)
+    n_frames = len(ftype)
+    seg_a = np.flatnonzero(ftype == 0)
+    seg_n = np.diff(np.r_[seg_a, n_frames]).astype(np.int64)
+    g = np.repeat(np.cumsum(ftype == 0) - 1, 3)          # segment of each plane
+    fg = np.repeat(np.arange(n_frames, dtype=np.int64), 3)
+    pp = np.tile(np.arange(3, dtype=np.int64), n_frames)
+    dest = 3 * seg_a[g] + pp * seg_n[g] + (fg - seg_a[g]) if n_frames else np.zeros(0, np.int64)
+    ch_g = np.repeat(np.arange(len(seg_a)), 3)
+    first = 3 * seg_a[ch_g] + np.tile(np.arange(3), len(seg_a)) * seg_n[ch_g]
+    count = seg_n[ch_g]
+    fr_at = np.concatenate([[0], np.cumsum(nf)])
+    ch_sid = np.searchsorted(fr_at, seg_a[ch_g], side="right") - 1
+    if len(ch_sid) and (np.asarray(hw)[ch_sid] == 0).any():
+        keep = np.asarray(hw)[ch_sid] > 0
+        first, count, ch_sid = first[keep], count[keep], ch_sid[keep]
+    return dest, first, count, ch_sid
+
+
+_PART_BYTES = 64 << 20   # coded bytes per decode part (H2D / decode overlap)
+_MAX_PARTS = 4
+_SIDE = {}
+
+
+def _split_parts(idx, sizes):
+    """Consecutive groups of `idx` with about equal bytes: one group below
+    _PART_BYTES, else up to _MAX_PARTS."""
+    total = sum(sizes)
+    n = min(_MAX_PARTS, len(idx), max(1, total // _PART_BYTES))
+    if n <= 1:
+        return [list(idx)]
+    parts, cur, acc, target = [], [], 0, total / n
+    for j, b in zip(idx, sizes):
+        cur.append(j)
+        acc += b
+        if acc >= target * (len(parts) + 1) and len(parts) < n - 1:
+            parts.append(cur)
+            cur = []
+    if cur:
+        parts.append(cur)
+    return parts
+
+
+def _side_streams(n):
+    dev = torch.cuda.current_device()
+    pool = _SIDE.setdefault(dev, [])
+    while len(pool) < n:
+        pool.append(torch.cuda.Stream(device=dev))
+    return pool[:n]
 
 
 def decode_frames(bs, cfg: CodecConfig, on_frame, stats=None):

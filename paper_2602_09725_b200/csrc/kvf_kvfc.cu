@@ -255,7 +255,94 @@ __device__ __forceinline__ bool mode_bit(const uint8_t* modes, int bw, int by, i
   return (modes[b >> 3] >> (7 - (b & 7))) & 1;  // np.packbits: MSB first
 }
 
-constexpr int kReconThreads = 512;
+constexpr int kReconThreads = 128;
+
+// ---- byte-lane (SWAR) helpers: four samples per 32-bit word, mod 256
+__device__ __forceinline__ uint32_t add_bytes(uint32_t a, uint32_t b) {
+  return ((a & 0x7F7F7F7Fu) + (b & 0x7F7F7F7Fu)) ^ ((a ^ b) & 0x80808080u);
+}
+__device__ __forceinline__ uint32_t unzig_bytes(uint32_t z) {  // per byte: (z>>1) ^ -(z&1)
+  return ((z >> 1) & 0x7F7F7F7Fu) ^ ((z & 0x01010101u) * 0xFFu);
+}
+__device__ __forceinline__ uint32_t bcast_byte(uint32_t b) { return (b & 0xFFu) * 0x01010101u; }
+// inclusive prefix sums mod 256 over the 16 bytes of q (byte 0 first)
+__device__ __forceinline__ uint4 prefix_bytes16(uint4 q) {
+  q.x = add_bytes(q.x, q.x << 8);
+  q.x = add_bytes(q.x, q.x << 16);
+  q.y = add_bytes(q.y, q.y << 8);
+  q.y = add_bytes(q.y, q.y << 16);
+  q.z = add_bytes(q.z, q.z << 8);
+  q.z = add_bytes(q.z, q.z << 16);
+  q.w = add_bytes(q.w, q.w << 8);
+  q.w = add_bytes(q.w, q.w << 16);
+  q.y = add_bytes(q.y, bcast_byte(q.x >> 24));
+  q.z = add_bytes(q.z, bcast_byte(q.y >> 24));
+  q.w = add_bytes(q.w, bcast_byte(q.z >> 24));
+  return q;
+}
+
+// One row of a plane, 16 samples per lane and 512 per warp step, when rows
+// are 16-B aligned and the width is a multiple of 16: vector loads/stores,
+// the next step's loads in flight while this step scans.  Column 0 (phase
+// A) is the row's initial carry; its symbol is dropped from an intra run.
+__device__ __forceinline__ void recon_row_vec(const uint8_t* sym, const uint8_t* prow,
+                                              uint8_t* orow, const uint8_t* modes, int bw,
+                                              int by, int w, uint32_t carry) {
+  const int lane = threadIdx.x & 31;
+  auto load = [&](int x0, uint4& sv, uint4& pv, bool& inter) {
+    const int xs = x0 + lane * 16;
+    sv = make_uint4(0u, 0u, 0u, 0u);
+    pv = sv;
+    inter = false;
+    if (xs < w) {
+      sv = __ldg(reinterpret_cast<const uint4*>(sym + xs));
+      inter = mode_bit(modes, bw, by, xs >> 4);
+      if (prow) pv = __ldcg(reinterpret_cast<const uint4*>(prow + xs));
+    }
+  };
+  uint4 sv, pv;
+  bool inter;
+  load(0, sv, pv, inter);
+  for (int x0 = 0; x0 < w; x0 += 32 * 16) {
+    uint4 sn, pn;
+    bool in_n;
+    load(x0 + 32 * 16, sn, pn, in_n);
+    const int xs = x0 + lane * 16;
+    uint4 d = make_uint4(unzig_bytes(sv.x), unzig_bytes(sv.y), unzig_bytes(sv.z),
+                         unzig_bytes(sv.w));
+    uint4 v;
+    Seg run;
+    if (inter) {
+      v = make_uint4(add_bytes(pv.x, d.x), add_bytes(pv.y, d.y), add_bytes(pv.z, d.z),
+                     add_bytes(pv.w, d.w));
+      run = Seg{1u, v.w >> 24};
+    } else {
+      if (xs == 0) d.x &= 0xFFFFFF00u;  // sample 0 = carry (phase A)
+      v = prefix_bytes16(d);
+      run = Seg{0u, v.w >> 24};
+    }
+    if (xs >= w) run = Seg{0u, 0u};
+    const Seg inc = warp_seg_scan(run);
+    Seg exc;
+    exc.abs = __shfl_up_sync(0xffffffffu, inc.abs, 1);
+    exc.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    const uint32_t before = lane > 0 ? (exc.abs ? exc.v : carry + exc.v) : carry;
+    if (!inter) {
+      const uint32_t b = bcast_byte(before);
+      v = make_uint4(add_bytes(v.x, b), add_bytes(v.y, b), add_bytes(v.z, b), add_bytes(v.w, b));
+    }
+    if (xs < w) *reinterpret_cast<uint4*>(orow + xs) = v;
+    const uint32_t last = inc.abs ? inc.v : carry + inc.v;
+    carry = __shfl_sync(0xffffffffu, last, 31);
+    sv = sn;
+    pv = pn;
+    inter = in_n;
+  }
+}
+
+__device__ __forceinline__ bool al16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
 
 __global__ void __launch_bounds__(kReconThreads)
     recon_kernel(const kvf_recon_plane* __restrict__ planes,
@@ -292,6 +379,17 @@ __global__ void __launch_bounds__(kReconThreads)
     }
     __syncthreads();
     // Phase B: each warp scans whole rows in spans of 32 runs x 16 pixels.
+    const bool vec = (w & 15) == 0 && al16(P.symbols) && al16(P.out) && (P.out_pitch & 15) == 0 &&
+                     (prev == nullptr || (al16(prev) && (prev_pitch & 15) == 0));
+    if (vec) {
+      for (int y = warp; y < h; y += nwarps) {
+        uint8_t* orow = P.out + (int64_t)y * P.out_pitch;
+        recon_row_vec(P.symbols + (int64_t)y * w, prev ? prev + (int64_t)y * prev_pitch : nullptr,
+                      orow, modes, bw, y >> 4, w, orow[0]);
+      }
+      __syncthreads();
+      continue;
+    }
     for (int y = warp; y < h; y += nwarps) {
       const uint8_t* sym = P.symbols + (int64_t)y * w;
       uint8_t* orow = P.out + (int64_t)y * P.out_pitch;

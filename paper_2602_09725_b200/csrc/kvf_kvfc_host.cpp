@@ -52,7 +52,11 @@ extern "C" kvf_status kvf_kvfc_scan(const uint8_t* data, int64_t size, kvf_kvfc_
   info->height = (int32_t)h;
   info->width = (int32_t)w;
   info->bitmap_len = (int32_t)blen;
-  const bool fill = cap_frames >= (int64_t)n;
+  if (cap_frames < (int64_t)n) {  // size query: the walk (and its checks) runs on the fill call
+    kvf::set_error("arrays hold %d frames, stream has %u", cap_frames, n);
+    return KVF_EINVAL;
+  }
+  const bool fill = true;
   int64_t pos = 12;
   for (int32_t f = 0; f < (int32_t)n; ++f) {
     if (pos >= size) return decode_error(bad_frame, f, "stream truncated");
@@ -81,9 +85,5 @@ extern "C" kvf_status kvf_kvfc_scan(const uint8_t* data, int64_t size, kvf_kvfc_
     }
   }
   if (pos != size) return decode_error(bad_frame, (int32_t)n - 1, "trailing bytes");
-  if (!fill) {
-    kvf::set_error("arrays hold %d frames, stream has %u", cap_frames, n);
-    return KVF_EINVAL;
-  }
   return KVF_OK;
 }

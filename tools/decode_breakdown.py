@@ -19,11 +19,11 @@ bs = codec.encode_batch([fr], [4])[0].data
 streams = [bs] * n_units
 if "--pinned" in sys.argv:
     streams = [torch.frombuffer(bytearray(bs), dtype=torch.uint8).pin_memory() for _ in range(n_units)]
-idx = [codec.StreamIndex(b) for b in streams]
+idx = codec.index_streams(streams)
 torch.cuda.synchronize()
 for rep in range(3):
     t0 = time.perf_counter()
-    ix = [codec.StreamIndex(b) for b in streams]
+    ix = codec.index_streams(streams)
     t1 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
