@@ -242,7 +242,8 @@ typedef struct kvf_rc_stream {
 
 /* Entropy-decode n_streams independent streams (fk/rangecoder.py:146-189:
  * adaptive order-0 model reset per stream, carry-less 32-bit range coder),
- * one GPU thread per stream.  `d_streams` is a DEVICE array. */
+ * one GPU thread per stream.  `d_streams` must be device-accessible: device
+ * memory or mapped (UVA) pinned host memory, read once per stream. */
 kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_streams,
                          void* stream);
 
@@ -266,7 +267,8 @@ typedef struct kvf_recon_chain {
 /* Reconstruct every chain (one CTA per chain; frames inside a chain in order):
  * sample = (pred + unzigzag(symbol)) mod 256 with pred = co-located previous
  * frame sample (inter block), left neighbour, first column from above, 128 at
- * the corner.  Both arrays are DEVICE arrays. */
+ * the corner.  Both arrays must be device-accessible: device memory or
+ * mapped (UVA) pinned host memory, read once per chain/plane. */
 kvf_status kvf_kvfc_reconstruct(const kvf_recon_plane* d_planes,
                                 const kvf_recon_chain* d_chains, int32_t n_chains,
                                 void* stream);

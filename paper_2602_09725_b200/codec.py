@@ -244,29 +244,31 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     for t in side:
         if t is not s:
             t.wait_stream(s)
-    base = blob.data_ptr()
-    done, keep = [], []
+    # every part's coded bytes go on the copy engine first ...
     for p, part in enumerate(parts):
-        t = side[p]
-        with torch.cuda.stream(t):
-            rc, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, base,
-                                                 symbols.data_ptr() + sym_at, frames)
-            d_rc, d_planes, d_chains = (
-                torch.from_numpy(np.ascontiguousarray(x if len(x) else np.zeros(1, x.dtype))
-                                 .view(np.uint8)).pin_memory().to(dev, non_blocking=True)
-                for x in (rc, flat, ch_arr))
+        with torch.cuda.stream(side[p]):
             for j in part:
                 lo, hi = spans[j]
                 s0 = int(starts[j])
                 src = datas[j][lo:hi] if pinned_in else host[s0:s0 + hi - lo]
                 blob[s0:s0 + hi - lo].copy_(src, non_blocking=True)
+    # ... then, part by part, the descriptors are built on the host while
+    # those copies run, and the kernels read them in place from pinned host
+    # memory (mapped, UVA): no H2D copy of their own to queue behind the bytes
+    base = blob.data_ptr()
+    done, keep = [], []
+    for p, part in enumerate(parts):
+        t = side[p]
+        rc, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, base,
+                                             symbols.data_ptr() + sym_at, frames)
+        h_rc, h_planes, h_chains = (_pinned_copy(x) for x in (rc, flat, ch_arr))
         sp = _dev.stream_ptr(t)
         if len(rc):
-            _lib.call("kvf_rc_decode", _dev.ptr(d_rc), len(rc), sp)
+            _lib.call("kvf_rc_decode", C.c_void_p(h_rc.data_ptr()), len(rc), sp)
         if len(ch_arr):
-            _lib.call("kvf_kvfc_reconstruct", _dev.ptr(d_planes), _dev.ptr(d_chains), len(ch_arr),
-                      sp)
-        keep += [d_rc, d_planes, d_chains]
+            _lib.call("kvf_kvfc_reconstruct", C.c_void_p(h_planes.data_ptr()),
+                      C.c_void_p(h_chains.data_ptr()), len(ch_arr), sp)
+        keep += [h_rc, h_planes, h_chains]
         if t is not s:
             ev = torch.cuda.Event()
             ev.record(t)
@@ -276,13 +278,38 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     if host is not None:
         _STAGING.release(s)   # `s` now follows every part's copies
     held = blob.numel() + symbols.numel() + sum(f.numel() for f in frames)
-    # keep descriptor/scratch tensors alive until the stream reaches this point
-    frames_keepalive = (blob, symbols, *keep, *frames)
+    # pinned descriptors: alive until `s` passes this point
+    _hold_until(s, keep)
+    # keep device scratch tensors alive until the stream reaches this point
+    frames_keepalive = (blob, symbols, *frames)
     for t in frames_keepalive:
         t.record_stream(s)
         for u, _ in done:
             t.record_stream(u)
     return frames, held
+
+
+_HELD = []   # (event, pinned host tensors) read by kernels not yet known complete
+_HELD_LOCK = threading.Lock()
+
+
+def _pinned_copy(a):
+    """A pinned host copy of numpy array `a` (at least one element), for a
+    kernel to read in place."""
+    a = np.ascontiguousarray(a if len(a) else np.zeros(1, a.dtype)).view(np.uint8)
+    t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+    t.numpy()[:] = a
+    return t
+
+
+def _hold_until(stream, tensors):
+    """Keep host tensors alive until `stream` passes this point (kernels on it
+    read them); drops the entries whose work completed."""
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    with _HELD_LOCK:
+        _HELD[:] = [(e, ts) for e, ts in _HELD if not e.query()]
+        _HELD.append((ev, tensors))
 
 
 def _part_descriptors(part, idxs, ranges, starts, spans, base, sym_ptr, frames):
@@ -365,8 +392,8 @@ def _chain_layout(ftype, nf, hw):
     return dest, first, count, ch_sid
 
 
-_PART_BYTES = 64 << 20   # coded bytes per decode part (H2D / decode overlap)
-_MAX_PARTS = 4
+_PART_BYTES = 32 << 20   # coded bytes per decode part (H2D / decode overlap)
+_MAX_PARTS = 8
 _SIDE = {}
 
 

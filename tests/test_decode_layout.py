@@ -51,8 +51,9 @@ def test_chain_layout_matches_definition(seed):
 def test_split_parts_balances_bytes():
     assert codec._split_parts([0, 1, 2], [10, 10, 10]) == [[0, 1, 2]]   # below one part
     big = codec._PART_BYTES
-    parts = codec._split_parts(list(range(8)), [big] * 8)
-    assert [j for p in parts for j in p] == list(range(8))
+    n = 2 * codec._MAX_PARTS
+    parts = codec._split_parts(list(range(n)), [big] * n)
+    assert [j for p in parts for j in p] == list(range(n))
     assert len(parts) == codec._MAX_PARTS and all(len(p) == 2 for p in parts)
     parts = codec._split_parts([3, 5], [5 * big, big])
     assert [j for p in parts for j in p] == [3, 5]
