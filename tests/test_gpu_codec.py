@@ -124,3 +124,35 @@ def test_rangecoder_module_matches_reference_golden(golden):
         assert ref.digest(enc) == c["coded"], c
         assert np.array_equal(RC.decode_bytes(enc, len(sym)), sym)
     assert len(RC.decode_bytes(b"", 5)) == 5   # reads past the end yield 0
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_part_pipeline_many_parts(monkeypatch, pinned):
+    """decode_batch split into the maximum number of parts (side streams,
+    descriptors read in place from pinned host memory), with partial frame
+    ranges, empty ranges and pitched outputs mixed in."""
+    monkeypatch.setattr(codec, "_PART_BYTES", 256)
+    rng = np.random.default_rng(9)
+    frames, streams, ranges = [], [], []
+    for i in range(40):
+        n = int(rng.integers(1, 9))
+        h, w = int(rng.integers(4, 33)), 16 * int(rng.integers(1, 6))
+        base = rng.integers(0, 256, size=(1, 3, h, w))
+        fr = np.clip(base + rng.integers(-5, 6, size=(n, 3, h, w)), 0, 255).astype(np.uint8)
+        gop = int(rng.integers(1, 4))
+        frames.append(fr)
+        bs = ref.encode_frames(fr, gop)
+        streams.append(torch.frombuffer(bytearray(bs), dtype=torch.uint8).pin_memory()
+                       if pinned else bs)
+        if i % 5 == 1:
+            ranges.append((0, 0))                       # nothing to decode
+        elif i % 5 == 2 and n > gop:
+            ranges.append((gop, n))                     # starts at the second intra frame
+        else:
+            ranges.append((0, n))
+    out, _ = codec.decode_batch(streams, ranges=ranges)
+    live = [j for j, (a, b) in enumerate(ranges) if b > a]
+    assert len(codec._split_parts(live, [1000] * len(live))) == codec._MAX_PARTS
+    for fr, (a, b), o in zip(frames, ranges, out):
+        assert tuple(o.shape) == (b - a,) + fr.shape[1:]
+        assert np.array_equal(o.cpu().numpy(), fr[a:b])

@@ -88,9 +88,10 @@ class ModelLink:
         code = resolution if isinstance(resolution, int) else L.RESOLUTION_CODE[resolution]
         meta, t = self.pinned[(bytes(cache_id), chunk_index, code)]
         self.sent += t.numel()
-        arrive = self.t0 + self.sent * 8 / self.rate
-        if arrive > now:
-            time.sleep(arrive - now)
+        if self.rate > 0:   # rate 0: no link limit (chunks handed over at once)
+            arrive = self.t0 + self.sent * 8 / self.rate
+            if arrive > now:
+                time.sleep(arrive - now)
         return t, meta, time.monotonic() - now
 
 
