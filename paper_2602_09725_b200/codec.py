@@ -13,6 +13,7 @@ Encode: see ``encode_frames`` (GPU residual/mode kernels + range coder).
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import struct
 import threading
@@ -226,9 +227,9 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     nf_all = np.array([f1 - f0 for f0, f1 in ranges], np.int64)
     sym_at = np.concatenate([[0], np.cumsum(3 * nf_all * hw16_all)])
     frames = []
+    blob = _scratch(s, "blob", int(starts[-1]) or 1)
+    symbols = _scratch(s, "symbols", max(int(sym_at[-1]), 1))
     with torch.cuda.stream(s):
-        blob = torch.empty(int(starts[-1]) or 1, dtype=torch.uint8, device=dev)
-        symbols = torch.empty(max(int(sym_at[-1]), 1), dtype=torch.uint8, device=dev)
         for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
             fr = out[j] if out is not None else torch.empty((f1 - f0, 3, ix.h, ix.w),
                                                            dtype=torch.uint8, device=dev)
@@ -287,6 +288,36 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
         for u, _ in done:
             t.record_stream(u)
     return frames, held
+
+
+_SCRATCH = collections.OrderedDict()   # (device, stream, name) -> grow-only device buffer
+_SCRATCH_STREAMS = 8
+_SCRATCH_LOCK = threading.Lock()
+
+
+def _scratch(stream, name, nbytes):
+    """Device scratch of `nbytes` reused across calls on `stream`.
+
+    Fresh cudaMallocs of varying sizes (a fetcher's batches differ) cost
+    15-40 ms each while the GPU is busy; a grow-only buffer per stream does
+    not.  Reuse is ordered: a call's kernels run on `stream` or on side
+    streams that `stream` waits for before returning, and the next call's
+    side streams wait for `stream` first.  Buffers of the least recently used
+    streams beyond _SCRATCH_STREAMS are dropped (their tensors carry
+    record_stream marks, so the allocator frees them safely).
+    """
+    key = (stream.device, stream.cuda_stream, name)
+    with _SCRATCH_LOCK:
+        t = _SCRATCH.get(key)
+        if t is None or t.numel() < nbytes:
+            with torch.cuda.stream(stream):
+                t = torch.empty(nbytes + nbytes // 4 + (1 << 20), dtype=torch.uint8,
+                                device=stream.device)
+            _SCRATCH[key] = t
+        _SCRATCH.move_to_end(key)
+        while len(_SCRATCH) > 2 * _SCRATCH_STREAMS:
+            _SCRATCH.popitem(last=False)
+    return t[:nbytes]
 
 
 _HELD = []   # (event, pinned host tensors) read by kernels not yet known complete

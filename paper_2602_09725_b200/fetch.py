@@ -15,6 +15,7 @@ from __future__ import annotations
 import json
 import os
 import queue
+import sys
 import threading
 import time
 from dataclasses import dataclass, field
@@ -205,6 +206,24 @@ class _PinnedPool:
 _RECEIVE_POOL = _PinnedPool()   # shared by every fetch of the process: pin once
 
 
+_WORKER_CTX = {}
+_WORKER_LOCK = threading.Lock()
+
+
+def _worker_context(slot):
+    """(CUDA stream, [frame buffer]) of GPU worker `slot` on the current
+    device, kept across fetches: the stream keys decode_batch's grow-only
+    scratch and the buffer holds a batch's decoded frames, so steady-state
+    fetches allocate no device memory (a cudaMalloc while the GPU is busy
+    costs 15-60 ms).  The lock serialises batches of concurrent fetches on a
+    slot; a batch synchronises before releasing it, so the buffer is free."""
+    key = (torch.cuda.current_device(), slot)
+    with _WORKER_LOCK:
+        if key not in _WORKER_CTX:
+            _WORKER_CTX[key] = (torch.cuda.Stream(), [None], threading.Lock())
+        return _WORKER_CTX[key]
+
+
 def _mem_for(mem, cache_id):
     return mem.get(cache_id, mem.get(cache_id.hex())) if isinstance(mem, dict) else mem
 
@@ -252,7 +271,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
     pool = _RECEIVE_POOL
     claim_lock = threading.Lock()   # PagedMemory host state + timeline bookkeeping
 
-    def run_batch(items, gpu_stream):
+    def run_batch(items, gpu_stream, frame_buf):
         t0 = time.monotonic()
         held = 0
         with torch.cuda.stream(gpu_stream):
@@ -260,7 +279,22 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 results = [NS.decode_fetched(meta, payload) for _, meta, payload in items]
             else:
                 conts = [NS.container_of(meta, b"") for _, meta, _ in items]
-                frames, held = codec.decode_batch([p for _, _, p in items], stream=gpu_stream)
+                payloads = [p for _, _, p in items]
+                idx = codec.index_streams(payloads)
+                # decoded frames in this worker's grow-only buffer: the batch is
+                # restored and synchronised before the next one reuses it
+                shapes = [(ix.n, 3, ix.h, ix.w) for ix in idx]
+                sizes = [n * 3 * h * w for n, _, h, w in shapes]
+                need = sum(-(-b // 256) * 256 for b in sizes)
+                if frame_buf[0] is None or frame_buf[0].numel() < need:
+                    frame_buf[0] = torch.empty(need + need // 4, dtype=torch.uint8,
+                                               device=gpu_stream.device)
+                out, at = [], 0
+                for shp, b in zip(shapes, sizes):
+                    out.append(frame_buf[0][at:at + b].view(shp))
+                    at += -(-b // 256) * 256
+                frames, held = codec.decode_batch(payloads, out=out, stream=gpu_stream,
+                                                  indices=idx)
                 t_dec = time.monotonic()
                 units = []
                 with claim_lock:  # claim every unit, then describe (pools may grow)
@@ -295,8 +329,8 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
             for (rec, _, _), res in zip(items, results):
                 on_chunk(rec, res)
 
-    def gpu_worker():
-        gpu_stream = torch.cuda.Stream()
+    def gpu_worker(slot):
+        gpu_stream, frame_buf, slot_lock = _worker_context(slot)
         while True:
             item = work.get()
             if item is None:
@@ -315,14 +349,20 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 items.append(nxt)
             try:
                 if not errors:
-                    run_batch(items, gpu_stream)
+                    with slot_lock:
+                        run_batch(items, gpu_stream, frame_buf)
             except Exception as e:  # surfaced on the caller's thread
                 errors.append(e)
             if stop:
                 return
 
-    pool_threads = [threading.Thread(target=gpu_worker, daemon=True)
-                    for _ in range(max(1, workers))]
+    pool_threads = [threading.Thread(target=gpu_worker, args=(k,), daemon=True)
+                    for k in range(max(1, workers))]
+    # The receive loop and the worker's host preparation share the GIL; with
+    # the default 5 ms switch interval a chunk that has arrived can wait that
+    # long for the loop to take it.  Use a short interval for the call.
+    switch = sys.getswitchinterval()
+    sys.setswitchinterval(min(switch, 0.0002))
     for t in pool_threads:
         t.start()
     history, active = [], initial_active
@@ -356,6 +396,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
         work.put(None)
         for t in pool_threads:
             t.join()
+        sys.setswitchinterval(switch)
     if errors:
         raise errors[0]
     timeline.ttft = state["dec_end"] if state["dec_end"] is not None else 0.0

@@ -17,6 +17,7 @@ the restored bf16 cache against dequantised codes.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import multiprocessing as mp
 import os
@@ -138,6 +139,13 @@ def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
         "host_restore_s": round(sum(r.get("host_restore_s", 0) for r in {r["decode_start"]: r for r in recs}.values()), 4),
         "gpu_busy_s": round(sum(r["tau_dec"] for r in {r["decode_start"]: r for r in recs}.values()), 4),
         "sampled_slots_mismatch": check(mems, qs, Lyr, args.tokens),
+        "max_receive_gap_s": round(max((b["transfer_start"] - a["transfer_end"]
+                                        for a, b in zip(recs, recs[1:])), default=0.0), 4),
+        "max_gap_before_chunk": max(range(1, len(recs)), default=0,
+                                    key=lambda i: recs[i]["transfer_start"] - recs[i - 1]["transfer_end"]),
+        "batches": [(round(r["decode_start"], 4), round(r["decode_end"], 4), r.get("batch"),
+                     round(r.get("host_decode_s", 0), 4), round(r.get("host_restore_s", 0), 4))
+                    for r in {r["decode_start"]: r for r in recs}.values()] if args.verbose else None,
         "setup_pack_s": round(setup_s, 1),
     }
     print(json.dumps(line), flush=True)
@@ -150,6 +158,7 @@ def main():
     ap.add_argument("--res", default="R240,R1080")
     ap.add_argument("--dir", default=None)
     ap.add_argument("--workers", type=int, default=1)
+    ap.add_argument("--verbose", action="store_true", help="per-batch timings in each line")
     ap.add_argument("--link", default="model", choices=["model", "tcp"],
                     help="model: constant-rate arrival replay; tcp: live loopback server")
     args = ap.parse_args()
@@ -178,12 +187,12 @@ def main():
             link = ModelLink(store, rate)
             link.stage(chunks, codes)
             mems = new_mems(qs, args.tokens, Lyr, H, D)
+            gc.collect()   # no collector pause inside the timed fetch
             torch.cuda.synchronize()
             tl = FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=rate, mem=mems,
                                         real_layers=Lyr, fetch_fn=link, workers=args.workers)
             emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, "modelled constant-rate link")
             del mems, link
-            torch.cuda.empty_cache()
         for rate in [float(r) for r in args.rates.split(",")] if args.link == "tcp" else []:
             # the chunk server runs in its own process (a remote node's role):
             # it does not share this process's GIL with the fetcher
@@ -202,7 +211,6 @@ def main():
             emit(tl, res, rate or None, coded, mems, qs, Lyr, args, setup_s,
                  "loopback TCP, reference wire protocol, token-bucket egress")
             del mems
-            torch.cuda.empty_cache()
     if args.dir is None:
         shutil.rmtree(root, ignore_errors=True)
 
