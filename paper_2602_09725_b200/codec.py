@@ -176,6 +176,7 @@ class _PinnedStaging:
 
 
 _STAGING = _PinnedStaging()
+_OUT_STAGING = _PinnedStaging()   # encode_batch's D2H of the coded streams
 
 
 def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
@@ -569,17 +570,26 @@ def encode_batch(frame_sets, gops, stream=None):
         pieces = np.concatenate(piece_parts) if piece_parts else np.zeros(1, _PIECE_DTYPE)
         _lib.call("kvf_gather", _dev.ptr(_to_dev_struct(pieces, dev)), len(pieces) if piece_parts else 0,
                   _dev.ptr(blob), sp)
-        host = blob.cpu().numpy()
-    results = []
-    for (base, size, n, h, w, frame_off, inter, len_off, ln, inter_frac) in layouts:
-        buf = host[base:base + size]      # header fields written in place, one copy out
-        buf[:12] = np.array([n, h, w], "<u4").view(np.uint8)
-        buf[frame_off] = inter.reshape(n, 3)[:, 0].astype(np.uint8) if n else buf[frame_off]
-        lb = ln.astype("<u4").view(np.uint8).reshape(-1, 4)
-        for b in range(4):
-            buf[len_off + b] = lb[:, b]
-        results.append(Bitstream(buf.tobytes(), n, h, w, [int(x) for x in frame_off], inter_frac))
-    return results
+        # one D2H into a reused pinned buffer (a fresh pageable one page-faults
+        # through the copy: ~2 GB/s), then one copy out per stream
+        out = _OUT_STAGING.acquire(max(total, 1))
+        try:
+            out.copy_(blob[:max(total, 1)], non_blocking=True)
+            s.synchronize()
+            return [_finish_stream(out.numpy(), *lay) for lay in layouts]
+        finally:
+            _OUT_STAGING.release(s)
+
+
+def _finish_stream(host, base, size, n, h, w, frame_off, inter, len_off, ln, inter_frac):
+    """Header fields of one encoded stream written in place, one copy out."""
+    buf = host[base:base + size]
+    buf[:12] = np.array([n, h, w], "<u4").view(np.uint8)
+    buf[frame_off] = inter.reshape(n, 3)[:, 0].astype(np.uint8) if n else buf[frame_off]
+    lb = ln.astype("<u4").view(np.uint8).reshape(-1, 4)
+    for b in range(4):
+        buf[len_off + b] = lb[:, b]
+    return Bitstream(buf.tobytes(), n, h, w, [int(x) for x in frame_off], inter_frac)
 
 
 def encode_frames(frames, cfg: CodecConfig) -> Bitstream:
