@@ -446,3 +446,52 @@ def test_wide_and_narrow_caches_pack_restore(H, D, gs):
     for t in (0, 17, T - 1):
         for p in range(3):
             assert torch.equal(mem.read(t, p).cpu(), deq[t, p].reshape(-1))
+
+
+@pytest.mark.parametrize("mode", ["twopass", "team"])
+def test_tiny_and_ragged_units_pack_then_restore(mode, monkeypatch):
+    """Units of 1..129 tokens (fewer tokens than F, partial last segments, one
+    token) in ONE kvf_pack_batch, then the GPU frames restored to int8 slots in
+    ONE restore batch: frames, scales and codes identical to the oracle."""
+    monkeypatch.setenv("KVF_PACK_MODE", mode)
+    from paper_2602_09725_b200 import _dev
+    specs = [(T, res, lay) for T in (1, 2, 3, 4, 5, 7, 15, 16, 17, 63, 64, 65, 129)
+             for res, lay in (("R240", (8, 128, 1, 8, 1, 128)), ("R1080", (8, 128, 2, 4, 16, 8)))]
+    units, keep, checks = [], [], []
+    for k, (T, res, lay) in enumerate(specs):
+        H, D = lay[0], lay[1]
+        x, v, s, want = _oracle_chunk(T, lay, res, seed=100 + k)
+        kv = np_bf16_from_f32(x.reshape(T, 3, H, D)).cuda()
+        plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+        fr = torch.full(plan.frame_shape(), 7, dtype=torch.uint8, device="cuda")  # not 128
+        am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(128)), dtype=torch.int32,
+                         device="cuda")
+        sc = torch.empty((3, H * D // 128), dtype=torch.float32, device="cuda")
+        u, _ = _pack_unit(kv, lay, res, 0, T, 4, 128, fr, am, sc)
+        units.append(u)
+        keep += [kv, am]
+        checks.append((T, lay, plan, v, s, want, fr, sc))
+    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * len(units))(*units), len(units), None)
+    torch.cuda.synchronize()
+    r_units, outs = [], []
+    for T, lay, plan, v, s, want, fr, sc in checks:
+        assert np.array_equal(sc.cpu().numpy(), s), (T, lay)
+        assert np.array_equal(fr.cpu().numpy(), want), (T, lay)
+        H, D = lay[0], lay[1]
+        out = [torch.zeros((T, H, D), dtype=torch.int8, device="cuda") for _ in range(3)]
+        dst = _lib.kvf_paged()
+        for p in range(3):
+            dst.layer[p] = out[p].data_ptr()
+        dst.block_table = None
+        dst.block_size = 1
+        dst.dtype = _lib.KVF_I8
+        dst.block_stride = dst.slot_stride = H * D
+        dst.head_stride = D
+        dst.token_base = 0
+        r_units.append(make_restore_unit(fr, plan, sc, dst, 128, 0, plan.frame_count))
+        outs.append(out)
+    restore_units(r_units)
+    torch.cuda.synchronize()
+    for (T, lay, plan, v, s, want, fr, sc), out in zip(checks, outs):
+        got = torch.stack([o.cpu() for o in out], 1).numpy().reshape(T, 3, -1)
+        assert np.array_equal(got, v.reshape(T, 3, -1)), (T, lay)
