@@ -121,25 +121,26 @@ __global__ void __launch_bounds__(kDecThreads)
     // cum is increasing in s, so both searches are binary over registers.
     const uint32_t x = code - low;
     // block: largest b with CB[b] * r <= x (CB[0] = 0 always qualifies)
-    const bool b3 = CB[8] * r <= x;
-    const bool b2 = (b3 ? CB[12] : CB[4]) * r <= x;
+    // The level-i operand is CB[(bits above) | 2^i]; CB[blk] is the operand of
+    // the last level that compared true (CB[0] = 0 if none), so `base` is a
+    // 4-select chain that finishes one select after b0.
+    const uint32_t o3 = CB[8];
+    const bool b3 = o3 * r <= x;
+    const uint32_t o2 = b3 ? CB[12] : CB[4];
+    const bool b2 = o2 * r <= x;
     const uint32_t c2a = b3 ? CB[10] : CB[2], c2b = b3 ? CB[14] : CB[6];
-    const bool b1 = (b2 ? c2b : c2a) * r <= x;
+    const uint32_t o1 = b2 ? c2b : c2a;
+    const bool b1 = o1 * r <= x;
     const uint32_t c1a = b3 ? CB[9] : CB[1], c1b = b3 ? CB[11] : CB[3];
     const uint32_t c1c = b3 ? CB[13] : CB[5], c1d = b3 ? CB[15] : CB[7];
     const uint32_t c1e = b2 ? c1c : c1a, c1f = b2 ? c1d : c1b;
-    const bool b0 = (b1 ? c1f : c1e) * r <= x;
+    const uint32_t o0 = b1 ? c1f : c1e;
+    const bool b0 = o0 * r <= x;
     const uint32_t blk = (b3 ? 8u : 0u) + (b2 ? 4u : 0u) + (b1 ? 2u : 0u) + (b0 ? 1u : 0u);
-    uint32_t base;
-    {
-      const uint32_t e0 = b3 ? CB[8] : CB[0], e1 = b3 ? CB[9] : CB[1];
-      const uint32_t e2 = b3 ? CB[10] : CB[2], e3 = b3 ? CB[11] : CB[3];
-      const uint32_t e4 = b3 ? CB[12] : CB[4], e5 = b3 ? CB[13] : CB[5];
-      const uint32_t e6 = b3 ? CB[14] : CB[6], e7 = b3 ? CB[15] : CB[7];
-      const uint32_t g0 = b2 ? e4 : e0, g1 = b2 ? e5 : e1, g2 = b2 ? e6 : e2, g3 = b2 ? e7 : e3;
-      const uint32_t h0 = b1 ? g2 : g0, h1 = b1 ? g3 : g1;
-      base = b0 ? h1 : h0;
-    }
+    uint32_t base = b3 ? o3 : 0u;
+    base = b2 ? o2 : base;
+    base = b1 ? o1 : base;
+    base = b0 ? o0 : base;
     const uint32_t rem = x - base * r;
     // within the block: incl[0..15] from two 128-bit loads
     const uint4 ca = m[(2 * blk) * kDecThreads], cb = m[(2 * blk + 1) * kDecThreads];
@@ -165,11 +166,11 @@ __global__ void __launch_bounds__(kDecThreads)
       const uint32_t pair = t1 ? p1 : p0;  // incl[sl'] | incl[sl' + 1] << 16
       i0 = lo16(pair);
       const bool t0 = i0 * r <= rem;
-      // value just below sl' (incl[sl' - 1]) : the high half of the previous word
-      const uint32_t pq0 = t3 ? wv[3] : 0u, pq1 = t3 ? wv[4] : wv[0];
-      const uint32_t pq2 = t3 ? wv[5] : wv[1], pq3 = t3 ? wv[6] : wv[2];
-      const uint32_t pp0 = t2 ? pq2 : pq0, pp1 = t2 ? pq3 : pq1;
-      const uint32_t below = hi16(t1 ? pp1 : pp0);     // incl[sl' - 1], 0 at sl' = 0
+      // incl[sl' - 1] (0 at sl' = 0) is the operand of the last of levels 3..1
+      // that compared true, as for `base`
+      uint32_t below = t3 ? i7 : 0u;
+      below = t2 ? i3 : below;
+      below = t1 ? i1 : below;
       lo_v = t0 ? i0 : below;
       hi_v = t0 ? hi16(pair) : i0;
       const uint32_t sl = (t3 ? 8u : 0u) + (t2 ? 4u : 0u) + (t1 ? 2u : 0u) + (t0 ? 1u : 0u);
