@@ -24,7 +24,13 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kIPW = 4;  // items per warp (loads in flight per lane: kIPW * VPL)
+constexpr int kIPW = 4;  // item rounds per warp (loads in flight per lane: kIPW * 4 or VPL)
+// Narrow slots (C = 256 / 512 channels: VPL 1 / 2 vectors per lane) put
+// SUB = 4 / VPL items side by side in a warp, 32 / SUB lanes each, so every
+// lane still moves 4 vectors per item round and the per-item index math is
+// amortised over as many bytes as for C = 1024.
+__host__ __device__ constexpr int sub_for(int vpl) { return vpl >= 4 ? 1 : 4 / vpl; }
+__host__ __device__ constexpr int ipw_for(int vpl) { return kIPW * sub_for(vpl); }
 
 struct RestoreUnitDev {
   kvf_surface fr;
@@ -52,29 +58,33 @@ __global__ void __launch_bounds__(kThreads)
   const int p = blockIdx.z;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int item0 = (blockIdx.x * kWarps + warp) * kIPW;
+  constexpr int SUB = sub_for(VPL);         // items side by side in the warp
+  constexpr int LPI = 32 / SUB;             // lanes per item
+  constexpr int VL = VPL * SUB;             // vectors per lane per item
+  const int sub = lane / LPI, sl = lane % LPI;
+  const int item0 = (blockIdx.x * kWarps + warp) * ipw_for(VPL);
   char* layer = reinterpret_cast<char*>(U.dst.layer[p]);
   if (item0 >= U.n_plane_items || layer == nullptr) return;
 
   constexpr int ES = OUT == KVF_F32 ? 4 : (OUT == KVF_I8 ? 1 : 2);
-  int32_t in_off[VPL];
-  int32_t out_off[VPL];
-  float s[VPL];
+  int32_t in_off[VL];
+  int32_t out_off[VL];
+  float s[VL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    int c = (lane + 32 * k) * 8;
+  for (int k = 0; k < VL; ++k) {
+    int c = (sl + LPI * k) * 8;
     in_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
     out_off[k] = (int32_t)slot_channel_offset(U.g, c, U.dst.head_stride) * ES;
     if constexpr (OUT != KVF_I8) s[k] = __ldg(U.scales + p * U.G + (c >> U.g.lg_gs));
   }
   const uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
 
-  uint2 v[kIPW][VPL];
+  uint2 v[kIPW][VL];
   char* outp[kIPW];
 #pragma unroll
   for (int it = 0; it < kIPW; ++it) {
     outp[it] = nullptr;
-    const int q = item0 + it;  // (frame, slot) item of this plane
+    const int q = item0 + it * SUB + sub;  // (frame, slot) item of this plane
     if (q < U.n_plane_items) {
       const int fl = fdiv(U.g.div_tpf, q);
       const int slot = q - fl * U.g.tpf;
@@ -86,7 +96,7 @@ __global__ void __launch_bounds__(kThreads)
         const uint8_t* src = plane_base + (int64_t)f * U.fr.frame_stride +
                              (int64_t)tr * U.g.tile_h * U.fr.row_pitch + tc * U.g.tile_w;
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) v[it][k] = ld_nc_v2(src + in_off[k]);
+        for (int k = 0; k < VL; ++k) v[it][k] = ld_nc_v2(src + in_off[k]);
         outp[it] = layer + paged_slot_offset_fd(U.dst, U.div_bs, i) * ES;
       }
     }
@@ -96,7 +106,7 @@ __global__ void __launch_bounds__(kThreads)
   for (int it = 0; it < kIPW; ++it) {
     if (outp[it] == nullptr) continue;
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
+    for (int k = 0; k < VL; ++k) {
       char* dst = outp[it] + out_off[k];
       if constexpr (OUT == KVF_I8) {
         // int8 code = u8 sample - 128 = sample ^ 0x80 (fk/fetchsim.py:351).
@@ -239,7 +249,7 @@ kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
       max_work = std::max(max_work, w);
     }
     if (max_work == 0) continue;
-    int64_t per_cta = vpl ? (int64_t)kWarps * kIPW : kThreads;
+    int64_t per_cta = vpl ? (int64_t)kWarps * ipw_for(vpl) : kThreads;
     int64_t gx = (max_work + per_cta - 1) / per_cta;
     if (gx > 0x7FFFFFFF) KVF_FAIL(KVF_EUNSUPPORTED, "restore grid too large");
     dim3 grid((unsigned)gx, (unsigned)n, 3);

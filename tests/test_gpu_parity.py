@@ -184,7 +184,10 @@ def _oracle_chunk(T, lay, res, seed, gs=128, F=4):
 
 @pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
                                  (8, 128, 2, 4, 16, 8), (8, 128, 1, 8, 128, 1),
-                                 (4, 8, 2, 2, 4, 2)])
+                                 (4, 8, 2, 2, 4, 2),
+                                 # 512- and 256-channel slots: 2 / 4 items side by side per warp
+                                 (4, 128, 1, 4, 1, 128), (4, 128, 2, 2, 8, 16),
+                                 (2, 128, 1, 2, 1, 128), (2, 128, 2, 1, 16, 8)])
 @pytest.mark.parametrize("dtype", [torch.int8, torch.bfloat16, torch.float16, torch.float32])
 def test_restore_paged_matches_oracle(lay, dtype):
     H, D = lay[0], lay[1]
