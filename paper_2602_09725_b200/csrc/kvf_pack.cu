@@ -30,6 +30,11 @@ constexpr int kWarps = kPackWarps;
 constexpr int kIPW = 8;         // frame items per warp (phase-split frames kernel)
 constexpr int kTokPerWarp = 8;  // absmax tokens per warp (phase-split absmax kernel)
 
+template <int SRC, int VPL>
+__host__ __device__ constexpr int pack_sub() {
+  return (SRC != KVF_I8 && VPL < 4) ? 4 / VPL : 1;
+}
+
 struct PackParams {
   int32_t n_units;
   PackUnitDev u[kMaxPackUnits];
@@ -131,15 +136,21 @@ __global__ void __launch_bounds__(kThreads, 4)
   const PackUnitDev& U = P.u[blockIdx.y];
   const int p = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item0 = (blockIdx.x * kWarps + warp) * kIPW;
+  // Narrow slots (VPL 1 / 2) run SUB items side by side, LPI lanes each, so a
+  // lane still handles 4 vectors per item round (as in restore).
+  constexpr int SUB = pack_sub<SRC, VPL>();
+  constexpr int LPI = 32 / SUB;
+  constexpr int VL = VPL * SUB;
+  const int sub = lane / LPI, sl = lane % LPI;
+  const int item0 = (blockIdx.x * kWarps + warp) * kIPW * SUB;
   if (item0 >= U.n_items) return;
   constexpr int ES = SRC == KVF_F32 ? 4 : (SRC == KVF_I8 ? 1 : 2);
   const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
-  int32_t in_off[VPL], tile_off[VPL];
-  float s[VPL], inv[VPL];
+  int32_t in_off[VL], tile_off[VL];
+  float s[VL], inv[VL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    int c = (lane + 32 * k) * 8;
+  for (int k = 0; k < VL; ++k) {
+    int c = (sl + LPI * k) * 8;
     in_off[k] = (int32_t)slot_channel_offset(U.g, c, U.src.head_stride) * ES;
     tile_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
     if constexpr (SRC != KVF_I8) {
@@ -170,20 +181,20 @@ __global__ void __launch_bounds__(kThreads, 4)
       locate(q, dst, slotp);
       if (slotp == nullptr) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k)
+        for (int k = 0; k < VL; ++k)
           st_v2(dst + tile_off[k], make_uint2(0x80808080u, 0x80808080u));
         continue;
       }
       if constexpr (SRC == KVF_I8) {
-        uint2 v[VPL];
+        uint2 v[VL];
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) v[k] = ld_nc_v2(slotp + in_off[k]);
+        for (int k = 0; k < VL; ++k) v[k] = ld_nc_v2(slotp + in_off[k]);
 #pragma unroll
-        for (int k = 0; k < VPL; ++k)
+        for (int k = 0; k < VL; ++k)
           st_v2(dst + tile_off[k], make_uint2(v[k].x ^ 0x80808080u, v[k].y ^ 0x80808080u));
       } else {
 #pragma unroll
-        for (int k0 = 0; k0 < VPL; k0 += 4) {  // at most 32 live values per lane
+        for (int k0 = 0; k0 < VL; k0 += 4) {  // at most 32 live values per lane
           float x[4][8];
 #pragma unroll
           for (int k = 0; k < 4; ++k) load_vec8<SRC>(slotp + in_off[k0 + k], x[k]);
@@ -196,35 +207,38 @@ __global__ void __launch_bounds__(kThreads, 4)
   } else {
     // Software pipeline: the loads of item it+1 are in flight while item it is
     // quantised and stored.
-    Raw8<SRC> cur[VPL], nxt[VPL];
+    Raw8<SRC> cur[VL], nxt[VL];
     uint8_t* dst_cur = nullptr;
     const char* src_cur = nullptr;
-    const int n_it = min(kIPW, U.n_items - item0);
-    locate(item0, dst_cur, src_cur);
+    const int n_it = min(kIPW, (U.n_items - item0 + SUB - 1) / SUB);  // warp-uniform rounds
+    if (SUB == 1 || item0 + sub < U.n_items) locate(item0 + sub, dst_cur, src_cur);
     if (src_cur)
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) cur[k] = load_raw8<SRC>(src_cur + in_off[k]);
+      for (int k = 0; k < VL; ++k) cur[k] = load_raw8<SRC>(src_cur + in_off[k]);
     for (int it = 0; it < n_it; ++it) {
       uint8_t* dst_nxt = nullptr;
       const char* src_nxt = nullptr;
-      if (it + 1 < n_it) {
-        locate(item0 + it + 1, dst_nxt, src_nxt);
+      const int qn = item0 + (it + 1) * SUB + sub;
+      if (it + 1 < n_it && (SUB == 1 || qn < U.n_items)) {
+        locate(qn, dst_nxt, src_nxt);
         if (src_nxt)
 #pragma unroll
-          for (int k = 0; k < VPL; ++k) nxt[k] = load_raw8<SRC>(src_nxt + in_off[k]);
+          for (int k = 0; k < VL; ++k) nxt[k] = load_raw8<SRC>(src_nxt + in_off[k]);
       }
+      if (SUB == 1 || dst_cur != nullptr) {  // SUB == 1: every round's item exists
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        uint2 out = make_uint2(0x80808080u, 0x80808080u);
-        if (src_cur) {
-          float x[8];
-          raw8_to_float<SRC>(cur[k], x);
-          out = quantize8<kRange>(x, s[k], inv[k]);
+        for (int k = 0; k < VL; ++k) {
+          uint2 out = make_uint2(0x80808080u, 0x80808080u);
+          if (src_cur) {
+            float x[8];
+            raw8_to_float<SRC>(cur[k], x);
+            out = quantize8<kRange>(x, s[k], inv[k]);
+          }
+          st_v2(dst_cur + tile_off[k], out);
         }
-        st_v2(dst_cur + tile_off[k], out);
       }
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) cur[k] = nxt[k];
+      for (int k = 0; k < VL; ++k) cur[k] = nxt[k];
       dst_cur = dst_nxt;
       src_cur = src_nxt;
     }
@@ -380,7 +394,8 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32
     if (quant && (phases & 4)) finalize_scales_kernel<<<dim3(1, (unsigned)n), 256, 0, s>>>(*P);
     if ((phases & 8) && max_items > 0) {
       if (vpl) {
-        int64_t per = (int64_t)kWarps * kIPW;
+        const int sub = (dtype != KVF_I8 && vpl < 4) ? 4 / vpl : 1;  // pack_sub<SRC, VPL>
+        int64_t per = (int64_t)kWarps * kIPW * sub;
         dim3 grid((unsigned)((max_items + per - 1) / per), (unsigned)n, 3);
         const bool trusted = (phases & 2) != 0;
         switch (dtype) {
