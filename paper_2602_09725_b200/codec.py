@@ -180,7 +180,8 @@ _OUT_STAGING = _PinnedStaging()   # encode_batch's D2H of the coded streams
 
 
 def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
-    """Decode many KVFC streams on the GPU in one pair of launches.
+    """Decode many KVFC streams on the GPU: two launches (range decode,
+    reconstruction) per part of up to _MAX_PARTS, pipelined with the H2D copy.
 
     ``streams``: list of bytes / Bitstream (staged through a reused pinned
     buffer), or of contiguous CPU uint8 tensors — pinned receive buffers —
@@ -189,7 +190,9 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     ``ranges``: optional per-stream (first, stop) frame range; ``first`` must
     be an intra frame (a chain start), and the output holds stop-first frames.
     Returns (frames list, device bytes held).  Raises DecodeError like the
-    reference.
+    reference.  The work is ordered on ``stream`` (default: current): callers
+    see the frames after it.  Calls on one stream must come from one thread
+    at a time (the device scratch is per stream).
     """
     dev = _dev.device()
     pinned_in = all(isinstance(x, torch.Tensor) for x in streams) and len(streams) > 0
@@ -237,11 +240,10 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
             if tuple(fr.shape) != (f1 - f0, 3, ix.h, ix.w):
                 raise ValueError("output frames have the wrong shape")
             frames.append(fr)
-    # Parts are pipelined on side streams: part p's descriptors and coded
-    # bytes are queued on the copy engine, then its two kernels; part p+1's
-    # host preparation and copies overlap part p's decoding.  (Every side
-    # stream first waits for the work `s` had before this call, so the memory
-    # allocated above on `s` is free.)
+    # Parts are pipelined on side streams: part p's two kernels follow its
+    # coded bytes on its stream, so they overlap the copies of parts p+1..
+    # (Every side stream first waits for the work `s` had before this call,
+    # so the memory allocated above on `s` is free.)
     side = _side_streams(len(parts)) if len(parts) > 1 else [s]
     for t in side:
         if t is not s:
