@@ -12,6 +12,7 @@ reference's bubble-minimising rule (fk/fetchsim.py:154-169).
 
 from __future__ import annotations
 
+import collections
 import json
 import os
 import queue
@@ -211,16 +212,17 @@ _WORKER_LOCK = threading.Lock()
 
 
 def _worker_context(slot):
-    """(CUDA stream, [frame buffer]) of GPU worker `slot` on the current
-    device, kept across fetches: the stream keys decode_batch's grow-only
-    scratch and the buffer holds a batch's decoded frames, so steady-state
-    fetches allocate no device memory (a cudaMalloc while the GPU is busy
-    costs 15-60 ms).  The lock serialises batches of concurrent fetches on a
-    slot; a batch synchronises before releasing it, so the buffer is free."""
+    """(CUDA stream, two [frame buffer] cells, lock) of GPU worker `slot` on
+    the current device, kept across fetches: the stream keys decode_batch's
+    grow-only scratch and the buffers hold the decoded frames of the two
+    batches a worker has in flight, so steady-state fetches allocate no device
+    memory (a cudaMalloc while the GPU is busy costs 15-60 ms).  A fetch's
+    worker holds the lock for its lifetime and drains its batches before
+    releasing it, so concurrent fetches on a slot take turns."""
     key = (torch.cuda.current_device(), slot)
     with _WORKER_LOCK:
         if key not in _WORKER_CTX:
-            _WORKER_CTX[key] = (torch.cuda.Stream(), [None], threading.Lock())
+            _WORKER_CTX[key] = (torch.cuda.Stream(), ([None], [None]), threading.Lock())
         return _WORKER_CTX[key]
 
 
@@ -271,9 +273,11 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
     pool = _RECEIVE_POOL
     claim_lock = threading.Lock()   # PagedMemory host state + timeline bookkeeping
 
-    def run_batch(items, gpu_stream, frame_buf):
+    def launch_batch(items, gpu_stream, frame_buf):
+        """Queue one batch's decode + restore on the worker stream; returns the
+        pending record that finish_batch completes once the GPU is done."""
         t0 = time.monotonic()
-        held = 0
+        held, t_dec, t_res = 0, t0, t0
         with torch.cuda.stream(gpu_stream):
             if mem is None:
                 results = [NS.decode_fetched(meta, payload) for _, meta, payload in items]
@@ -281,8 +285,8 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 conts = [NS.container_of(meta, b"") for _, meta, _ in items]
                 payloads = [p for _, _, p in items]
                 idx = codec.index_streams(payloads)
-                # decoded frames in this worker's grow-only buffer: the batch is
-                # restored and synchronised before the next one reuses it
+                # decoded frames in one of this worker's two grow-only buffers:
+                # a buffer is reused only after the batch two back completed
                 shapes = [(ix.n, 3, ix.h, ix.w) for ix in idx]
                 sizes = [n * 3 * h * w for n, _, h, w in shapes]
                 need = sum(-(-b // 256) * 256 for b in sizes)
@@ -308,14 +312,19 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                     restore_units(units, stream=gpu_stream)
                 t_res = time.monotonic()
                 results = [{"tokens_written": u.tokens_written} for u in units]
-            done = torch.cuda.Event()
+            done = torch.cuda.Event(enable_timing=True)
             done.record(gpu_stream)
         pool.put([p for _, _, p in items if isinstance(p, torch.Tensor)], done)
-        gpu_stream.synchronize()
-        t1 = time.monotonic()
+        return {"items": items, "results": results, "held": held, "done": done,
+                "t0": t0, "t_dec": t_dec, "t_res": t_res}
+
+    def finish_batch(b, clock):
+        b["done"].synchronize()
+        t0, t1 = b["t0"], clock(b["done"])   # when the GPU finished the batch
+        items = b["items"]
         with claim_lock:
-            host = {} if mem is None else {"host_decode_s": t_dec - t0,
-                                           "host_restore_s": t_res - t_dec}
+            host = {} if mem is None else {"host_decode_s": b["t_dec"] - t0,
+                                           "host_restore_s": b["t_res"] - b["t_dec"]}
             for rec, _, _ in items:
                 rec.update(decode_start=t0 - base, decode_end=t1 - base, tau_dec=t1 - t0,
                            batch=len(items), **host)
@@ -324,37 +333,59 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 items[0][0]["bubble"] = bubble
                 timeline.total_bubble += bubble
             state["dec_end"] = max(t1 - base, state["dec_end"] or 0.0)
-            timeline.peak_restore_bytes = max(timeline.peak_restore_bytes, held)
+            timeline.peak_restore_bytes = max(timeline.peak_restore_bytes, b["held"])
         if on_chunk is not None:
-            for (rec, _, _), res in zip(items, results):
+            for (rec, _, _), res in zip(items, b["results"]):
                 on_chunk(rec, res)
 
     def gpu_worker(slot):
-        gpu_stream, frame_buf, slot_lock = _worker_context(slot)
-        while True:
-            item = work.get()
-            if item is None:
-                work.put(None)  # let the other workers see the end too
-                return
-            items, stop = [item], False
-            while len(items) < max_batch:
-                try:
-                    nxt = work.get_nowait()
-                except queue.Empty:
-                    break
-                if nxt is None:
-                    stop = True
-                    work.put(None)
-                    break
-                items.append(nxt)
+        """Takes every chunk received so far as one batch and queues it while
+        the previous batch still runs on the GPU (at most two in flight), so
+        the host preparation of batch k+1 overlaps the GPU work of batch k."""
+        gpu_stream, frame_bufs, slot_lock = _worker_context(slot)
+        with slot_lock:  # concurrent fetches on this slot take turns
+            with torch.cuda.stream(gpu_stream):
+                ref_ev = torch.cuda.Event(enable_timing=True)
+                ref_ev.record(gpu_stream)
+            ref_ev.synchronize()
+            ref_t = time.monotonic()
+
+            def clock(ev):  # host time at which the GPU reached event `ev`
+                return ref_t + ref_ev.elapsed_time(ev) / 1e3
+
+            inflight, k, stop = collections.deque(), 0, False
             try:
-                if not errors:
-                    with slot_lock:
-                        run_batch(items, gpu_stream, frame_buf)
+                while not stop:
+                    while inflight and inflight[0]["done"].query():
+                        finish_batch(inflight.popleft(), clock)
+                    try:
+                        item = work.get(timeout=0.0005) if inflight else work.get()
+                    except queue.Empty:
+                        continue
+                    if item is None:
+                        work.put(None)  # let the other workers see the end too
+                        break
+                    items = [item]
+                    while len(items) < max_batch:
+                        try:
+                            nxt = work.get_nowait()
+                        except queue.Empty:
+                            break
+                        if nxt is None:
+                            stop = True
+                            work.put(None)
+                            break
+                        items.append(nxt)
+                    if errors:
+                        continue
+                    if len(inflight) == 2:  # its frame buffer is the one reused next
+                        finish_batch(inflight.popleft(), clock)
+                    inflight.append(launch_batch(items, gpu_stream, frame_bufs[k % 2]))
+                    k += 1
+                while inflight:
+                    finish_batch(inflight.popleft(), clock)
             except Exception as e:  # surfaced on the caller's thread
                 errors.append(e)
-            if stop:
-                return
 
     pool_threads = [threading.Thread(target=gpu_worker, args=(k,), daemon=True)
                     for k in range(max(1, workers))]
