@@ -28,7 +28,9 @@ namespace {
 constexpr int kThreads = kPackThreads;
 constexpr int kWarps = kPackWarps;
 constexpr int kIPW = 8;         // frame items per warp (phase-split frames kernel)
-constexpr int kTokPerWarp = 8;  // absmax tokens per warp (phase-split absmax kernel)
+// absmax tokens per warp (phase-split absmax kernel): 8 for C >= 1024 channels,
+// more for narrow slots so a CTA still reads ~128 KB
+__host__ __device__ constexpr int tok_per_warp(int vpl) { return vpl >= 4 ? 8 : 32 / vpl; }
 
 template <int SRC, int VPL>
 __host__ __device__ constexpr int pack_sub() {
@@ -75,6 +77,7 @@ __global__ void __launch_bounds__(kThreads)
   const PackUnitDev& U = P.u[blockIdx.y];
   const int p = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kTokPerWarp = tok_per_warp(VPL);
   const int tok0 = (blockIdx.x * kWarps + warp) * kTokPerWarp;
   const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
   if (blockIdx.x * kWarps * kTokPerWarp >= U.g.T || layer == nullptr) return;
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(kThreads)
     off[k] = (int32_t)slot_channel_offset(U.g, (lane + 32 * k) * 8, U.src.head_stride) * ES;
     m[k] = 0u;
   }
-#pragma unroll 2
+#pragma unroll(VPL >= 4 ? 2 : 8 / VPL)  // ~8 vectors per lane in flight
   for (int t = 0; t < kTokPerWarp; ++t) {
     int i = tok0 + t;
     if (i >= U.g.T) break;
@@ -378,7 +381,7 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32
     if (quant && (phases & 1)) zero_absmax_kernel<<<dim3(1, (unsigned)n), 256, 0, s>>>(*P);
     if (quant && (phases & 2) && max_T > 0) {
       if (vpl) {
-        int64_t per = (int64_t)kWarps * kTokPerWarp;
+        int64_t per = (int64_t)kWarps * tok_per_warp(vpl);
         dim3 grid((unsigned)((max_T + per - 1) / per), (unsigned)n, 3);
         switch (dtype) {
           case KVF_BF16: launch_absmax_fast<KVF_BF16>(vpl, *P, grid, smem, s); break;
