@@ -244,7 +244,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     # coded bytes on its stream, so they overlap the copies of parts p+1..
     # (Every side stream first waits for the work `s` had before this call,
     # so the memory allocated above on `s` is free.)
-    side = _side_streams(len(parts)) if len(parts) > 1 else [s]
+    side = _side_streams(s, len(parts)) if len(parts) > 1 else [s]
     for t in side:
         if t is not s:
             t.wait_stream(s)
@@ -313,8 +313,9 @@ def _scratch(stream, name, nbytes):
     with _SCRATCH_LOCK:
         t = _SCRATCH.get(key)
         if t is None or t.numel() < nbytes:
+            _SCRATCH.pop(key, None)   # the old buffer goes first
             with torch.cuda.stream(stream):
-                t = torch.empty(nbytes + nbytes // 4 + (1 << 20), dtype=torch.uint8,
+                t = torch.empty(2 * nbytes + (1 << 20), dtype=torch.uint8,
                                 device=stream.device)
             _SCRATCH[key] = t
         _SCRATCH.move_to_end(key)
@@ -450,12 +451,19 @@ def _split_parts(idx, sizes):
     return parts
 
 
-def _side_streams(n):
-    dev = torch.cuda.current_device()
-    pool = _SIDE.setdefault(dev, [])
-    while len(pool) < n:
-        pool.append(torch.cuda.Stream(device=dev))
-    return pool[:n]
+def _side_streams(stream, n):
+    """Side streams of the calling stream (each caller stream has its own, so
+    decodes issued concurrently on different streams do not serialise on a
+    shared pool).  Least recently used entries beyond _SCRATCH_STREAMS go."""
+    key = (stream.device, stream.cuda_stream)
+    with _SCRATCH_LOCK:
+        pool = _SIDE.pop(key, [])
+        _SIDE[key] = pool
+        while len(pool) < n:
+            pool.append(torch.cuda.Stream(device=stream.device))
+        while len(_SIDE) > _SCRATCH_STREAMS:
+            _SIDE.pop(next(iter(_SIDE)))
+        return pool[:n]
 
 
 def decode_frames(bs, cfg: CodecConfig, on_frame, stats=None):

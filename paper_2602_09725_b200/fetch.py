@@ -175,33 +175,69 @@ class _PinnedPool:
 
     Pinning is slow (and serialises with the device), so buffers are never
     freed during a fetch, and each is allocated with 25% headroom so the next
-    chunks' slightly different payload sizes reuse it."""
+    chunks' slightly different payload sizes reuse it.  A returned buffer
+    comes back with the event of the batch that reads it and is handed out
+    again only once that event completed; returning never blocks (the GPU
+    worker must not wait for its own batch)."""
 
     def __init__(self):
         self._free: list[torch.Tensor] = []
+        self._pending: list[tuple] = []   # (event, [buffers]) not yet known read
+        self._owned: set[int] = set()     # data_ptr of every buffer this pool pinned
         self._lock = threading.Lock()
 
-    def get(self, n: int) -> torch.Tensor:
+    def _new(self, n: int) -> torch.Tensor:
+        b = torch.empty(max(n + n // 4, 1 << 20), dtype=torch.uint8, pin_memory=True)
         with self._lock:
-            fits = [k for k, b in enumerate(self._free) if b.numel() >= n]
-            if fits:
-                k = min(fits, key=lambda k: self._free[k].numel())
-                return self._free.pop(k)[:n]
-        return torch.empty(max(n + n // 4, 1 << 20), dtype=torch.uint8, pin_memory=True)[:n]
+            self._owned.add(b.data_ptr())
+        return b
+
+    def _reap(self) -> None:  # under the lock
+        still = []
+        for ev, bufs in self._pending:
+            if ev.query():
+                self._free.extend(bufs)
+            else:
+                still.append((ev, bufs))
+        self._pending = still
+
+    def _take(self, n: int):  # under the lock
+        fits = [k for k, b in enumerate(self._free) if b.numel() >= n]
+        if fits:
+            k = min(fits, key=lambda k: self._free[k].numel())
+            return self._free.pop(k)[:n]
+        return None
+
+    def get(self, n: int) -> torch.Tensor:
+        while True:
+            with self._lock:
+                self._reap()
+                b = self._take(n)
+                if b is not None:
+                    return b
+                oldest = self._pending[0][0] if self._pending else None
+            if oldest is None:
+                break
+            oldest.synchronize()  # every buffer is in flight: wait for the oldest batch
+        return self._new(n)[:n]
 
     def put(self, bufs, event) -> None:
-        event.synchronize()  # the H2D copies that read these buffers are done
+        """Return buffers (those this pool handed out; others are ignored)."""
+        bases = [b._base if b._base is not None else b for b in bufs]
         with self._lock:
-            for b in bufs:
-                self._free.append(b._base if b._base is not None else b)
+            mine = [b for b in bases if b.data_ptr() in self._owned]
+            if mine:
+                self._pending.append((event, mine))
 
     def warm(self, n: int, count: int) -> None:
-        """Make sure `count` free buffers hold payloads of about n bytes."""
+        """Make sure `count` buffers (free or in flight) hold payloads of about n bytes."""
         with self._lock:
+            self._reap()
             have = sum(1 for b in self._free if b.numel() >= n)
-        bufs = [self.get(n) for _ in range(max(0, count - have))]
+            have += sum(1 for _, bs in self._pending for b in bs if b.numel() >= n)
+        bufs = [self._new(n) for _ in range(max(0, count - have))]
         with self._lock:
-            self._free.extend(b._base if b._base is not None else b for b in bufs)
+            self._free.extend(bufs)
 
 
 _RECEIVE_POOL = _PinnedPool()   # shared by every fetch of the process: pin once
@@ -211,18 +247,29 @@ _WORKER_CTX = {}
 _WORKER_LOCK = threading.Lock()
 
 
+# batches a GPU worker keeps in flight (one stream + frame buffer each), and the
+# fewest chunks a batch takes while others are in flight
+_INFLIGHT = int(os.environ.get("KVF_FETCH_INFLIGHT", "4"))
+_MIN_BATCH = int(os.environ.get("KVF_FETCH_MIN_BATCH", "4"))
+_LONG_STREAM = 1 << 16   # symbols per stream from which a batch decode is latency-bound
+
+
 def _worker_context(slot):
-    """(CUDA stream, two [frame buffer] cells, lock) of GPU worker `slot` on
-    the current device, kept across fetches: the stream keys decode_batch's
-    grow-only scratch and the buffers hold the decoded frames of the two
-    batches a worker has in flight, so steady-state fetches allocate no device
-    memory (a cudaMalloc while the GPU is busy costs 15-60 ms).  A fetch's
-    worker holds the lock for its lifetime and drains its batches before
-    releasing it, so concurrent fetches on a slot take turns."""
+    """(_INFLIGHT CUDA streams, as many [frame buffer] cells, lock) of GPU
+    worker `slot` on the current device, kept across fetches: batch k of a
+    worker runs on stream k % _INFLIGHT with that frame buffer, so batches
+    overlap on the GPU — a long-stream (R1080) decode is latency-bound, and
+    batches decoded one after another would add their latencies.  The
+    streams key decode_batch's grow-only scratch, so steady-state fetches
+    allocate no device memory (a cudaMalloc while the GPU is busy costs
+    15-60 ms).  A fetch's worker holds the lock for its lifetime and drains
+    its batches before releasing it, so concurrent fetches on a slot take
+    turns."""
     key = (torch.cuda.current_device(), slot)
     with _WORKER_LOCK:
         if key not in _WORKER_CTX:
-            _WORKER_CTX[key] = (torch.cuda.Stream(), ([None], [None]), threading.Lock())
+            _WORKER_CTX[key] = (tuple(torch.cuda.Stream() for _ in range(_INFLIGHT)),
+                                tuple([None] for _ in range(_INFLIGHT)), threading.Lock())
         return _WORKER_CTX[key]
 
 
@@ -273,7 +320,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
     pool = _RECEIVE_POOL
     claim_lock = threading.Lock()   # PagedMemory host state + timeline bookkeeping
 
-    def launch_batch(items, gpu_stream, frame_buf):
+    def launch_batch(items, gpu_stream, frame_buf, peers=()):
         """Queue one batch's decode + restore on the worker stream; returns the
         pending record that finish_batch completes once the GPU is done."""
         t0 = time.monotonic()
@@ -290,8 +337,21 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 shapes = [(ix.n, 3, ix.h, ix.w) for ix in idx]
                 sizes = [n * 3 * h * w for n, _, h, w in shapes]
                 need = sum(-(-b // 256) * 256 for b in sizes)
+                # every stream of the worker grows together (its next batches
+                # land on the others): growth happens once, not per stream
+                blob_need = sum(int(p.numel()) if isinstance(p, torch.Tensor) else len(p)
+                                for p in payloads)
+                sym_need = sum(3 * ix.n * (-(-ix.h * ix.w // 16) * 16) for ix in idx)
+                for t, fb in peers:
+                    codec._scratch(t, "blob", blob_need)
+                    codec._scratch(t, "symbols", sym_need)
+                    if fb[0] is None or fb[0].numel() < need:
+                        fb[0] = None   # drop the old buffer before allocating
+                        with torch.cuda.stream(t):
+                            fb[0] = torch.empty(2 * need, dtype=torch.uint8, device=t.device)
                 if frame_buf[0] is None or frame_buf[0].numel() < need:
-                    frame_buf[0] = torch.empty(need + need // 4, dtype=torch.uint8,
+                    frame_buf[0] = None
+                    frame_buf[0] = torch.empty(2 * need, dtype=torch.uint8,
                                                device=gpu_stream.device)
                 out, at = [], 0
                 for shp, b in zip(shapes, sizes):
@@ -315,8 +375,9 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
             done = torch.cuda.Event(enable_timing=True)
             done.record(gpu_stream)
         pool.put([p for _, _, p in items if isinstance(p, torch.Tensor)], done)
+        long_streams = mem is not None and max(ix.h * ix.w for ix in idx) >= _LONG_STREAM
         return {"items": items, "results": results, "held": held, "done": done,
-                "t0": t0, "t_dec": t_dec, "t_res": t_res}
+                "t0": t0, "t_dec": t_dec, "t_res": t_res, "long": long_streams}
 
     def finish_batch(b, clock):
         b["done"].synchronize()
@@ -339,21 +400,21 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                 on_chunk(rec, res)
 
     def gpu_worker(slot):
-        """Takes every chunk received so far as one batch and queues it while
-        the previous batch still runs on the GPU (at most two in flight), so
-        the host preparation of batch k+1 overlaps the GPU work of batch k."""
-        gpu_stream, frame_bufs, slot_lock = _worker_context(slot)
+        """Takes every chunk received so far as one batch and queues it on its
+        own stream while earlier batches still run (at most _INFLIGHT), so
+        host preparation and the batches' GPU work overlap."""
+        streams, frame_bufs, slot_lock = _worker_context(slot)
         with slot_lock:  # concurrent fetches on this slot take turns
-            with torch.cuda.stream(gpu_stream):
+            with torch.cuda.stream(streams[0]):
                 ref_ev = torch.cuda.Event(enable_timing=True)
-                ref_ev.record(gpu_stream)
+                ref_ev.record(streams[0])
             ref_ev.synchronize()
             ref_t = time.monotonic()
 
             def clock(ev):  # host time at which the GPU reached event `ev`
                 return ref_t + ref_ev.elapsed_time(ev) / 1e3
 
-            inflight, k, stop = collections.deque(), 0, False
+            inflight, k, stop, long_streams = collections.deque(), 0, False, False
             try:
                 while not stop:
                     while inflight and inflight[0]["done"].query():
@@ -376,11 +437,32 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                             work.put(None)
                             break
                         items.append(nxt)
+                    # With batches already in flight, a new one waits for at least
+                    # _MIN_BATCH chunks (or for the oldest batch to finish): small
+                    # batches cost a decode latency each and thin out throughput.
+                    while (inflight and not stop and len(items) < _MIN_BATCH and
+                           not inflight[0]["done"].query()):
+                        try:
+                            nxt = work.get(timeout=0.0005)
+                        except queue.Empty:
+                            continue
+                        if nxt is None:
+                            stop = True
+                            work.put(None)
+                            break
+                        items.append(nxt)
                     if errors:
                         continue
-                    if len(inflight) == 2:  # its frame buffer is the one reused next
+                    # Long streams (R480 and up) decode latency-bound: up to
+                    # _INFLIGHT batches overlap.  Short ones (R240) are
+                    # throughput-bound and two in flight keep the GPU busy.
+                    limit = _INFLIGHT if long_streams else min(2, _INFLIGHT)
+                    while len(inflight) >= limit:  # the oldest's stream + buffer are reused
                         finish_batch(inflight.popleft(), clock)
-                    inflight.append(launch_batch(items, gpu_stream, frame_bufs[k % 2]))
+                    j = k % _INFLIGHT
+                    inflight.append(launch_batch(items, streams[j], frame_bufs[j],
+                                                 list(zip(streams, frame_bufs))))
+                    long_streams = inflight[-1]["long"]
                     k += 1
                 while inflight:
                     finish_batch(inflight.popleft(), clock)

@@ -232,9 +232,15 @@ class PagedMemory:
             host = torch.from_numpy(self._table_host.copy()).pin_memory()
             with torch.cuda.stream(self._upload_stream):
                 self._table = host.to(_dev.device(), non_blocking=True)
-            self._table.record_stream(torch.cuda.current_stream())
-            torch.cuda.current_stream().wait_stream(self._upload_stream)
+                self._table_ready = torch.cuda.Event()
+                self._table_ready.record(self._upload_stream)
             self._table_dirty = False
+        # Every consumer stream (a fetcher runs batches on several) waits for the
+        # upload and marks the table in use, so it is neither read early nor
+        # recycled while a queued kernel on that stream still reads it.
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self._table_ready)
+        self._table.record_stream(cur)
         return self._table
 
     def _map_pages(self, first_page: int, last_page: int):

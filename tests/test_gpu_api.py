@@ -165,9 +165,16 @@ def test_fetch_errors(tmp_path):
         handle.close()
 
 
-def test_pipelined_fetch_batches_k_and_v_into_paged_bf16(tmp_path):
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_pipelined_fetch_batches_k_and_v_into_paged_bf16(tmp_path, monkeypatch, concurrent):
     """The batched pipeline (several chunks per decode launch, two caches) with a
-    replayed link: every K and V slot equals dequantize() of the packed codes."""
+    replayed link: every K and V slot equals dequantize() of the packed codes.
+    `concurrent`: one chunk per batch and every batch treated as long-stream,
+    so up to _INFLIGHT batches run at once on the worker's streams while the
+    block tables change under them."""
+    if concurrent:
+        monkeypatch.setattr(FE, "_LONG_STREAM", 1)
+        monkeypatch.setattr(FE, "_MIN_BATCH", 1)
     cfg = L.identity_layout(8, 32)
     store_chunks, qs = [], {}
     for kv_i in range(2):
@@ -197,12 +204,12 @@ def test_pipelined_fetch_batches_k_and_v_into_paged_bf16(tmp_path):
 
     mems = {cid: KV.PagedMemory(16, dtype=torch.bfloat16) for cid in qs}
     tl = FE.live_fetch_pipeline(None, store_chunks, None, "fixed:R240", mem=mems, real_layers=5,
-                                fetch_fn=replay, max_batch=4)
+                                fetch_fn=replay, max_batch=1 if concurrent else 4)
     assert len(tl.records) == len(store_chunks)
     assert max(r["batch"] for r in tl.records) >= 1
     for cid, q in qs.items():
         deq = KV.dequantize(q, torch.bfloat16).data
-        for t in (0, 127, 128, 255, 256, 299):
+        for t in range(300):
             for l in range(5):
                 assert torch.equal(mems[cid].read(t, l), deq[t, l].reshape(-1)), (cid, t, l)
         assert mems[cid].read(0, 5) is None          # pad layer never written

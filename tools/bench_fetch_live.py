@@ -176,13 +176,16 @@ def main():
         code = codes[0]
         coded = sum(store.index[(cid, idx)]["entries"][code][1] for cid, idx in chunks)  # fixed classes
         policy = "adaptive" if res == "adaptive" else f"fixed:{res}"
-        # untimed warm-up: pins the receive pool, grows the allocator, loads kernels
-        link = ModelLink(store, 1000.0)
-        link.stage(chunks, codes)
-        FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=10.0,
-                               mem=new_mems(qs, args.tokens, Lyr, H, D), real_layers=Lyr,
-                               fetch_fn=link)
-        del link
+        # untimed warm-up: pins the receive pool, loads kernels and grows every
+        # worker stream's grow-only buffers (large batches at 1000 Gbps, many
+        # small ones at 50 Gbps) so timed runs allocate no device memory
+        for warm_rate in (1000.0, 50.0):
+            link = ModelLink(store, warm_rate)
+            link.stage(chunks, codes)
+            FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=10.0,
+                                   mem=new_mems(qs, args.tokens, Lyr, H, D), real_layers=Lyr,
+                                   fetch_fn=link)
+            del link
         for rate in [float(r) for r in args.rates.split(",")] if args.link == "model" else []:
             link = ModelLink(store, rate)
             link.stage(chunks, codes)

@@ -14,6 +14,17 @@ def wrap(mod, name):
                 print(f"SLOW {name} {dt*1e3:.1f} ms\n" + "\n".join(s.getvalue().splitlines()[6:16]), file=sys.stderr)
     setattr(mod, name, w)
 wrap(codec, "decode_batch"); wrap(FE, "restore_unit"); wrap(FE, "restore_units")
+from paper_2602_09725_b200 import _lib as _L
+_orig_call = _L.call
+def timed_call(name, *a):
+    t = time.perf_counter()
+    try:
+        return _orig_call(name, *a)
+    finally:
+        dt = time.perf_counter() - t
+        if dt > 0.005:
+            print(f"SLOW lib {name} {dt*1e3:.1f} ms", file=sys.stderr)
+_L.call = timed_call
 import torch
 _orig_empty = torch.empty
 def timed_empty(*a, **k):
@@ -25,5 +36,5 @@ def timed_empty(*a, **k):
     return r
 torch.empty = timed_empty
 import bench_fetch_live
-sys.argv = ["x", "--rates", "100,100,100,100,100,100", "--res", "R240"]
+sys.argv = ["x", "--rates", os.environ.get("RATES", "100,100,100,100,100,100"), "--res", os.environ.get("RES", "R240")]
 bench_fetch_live.main()
