@@ -91,6 +91,8 @@ struct ByteWindow {
 __global__ void __launch_bounds__(kDecThreads)
     rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n) {
   extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B
+  __shared__ uint4 T_add[32];  // in-block increment rows (rc::add_table_init)
+  add_table_init(T_add);       // the whole warp, before any thread leaves
   const int tid = threadIdx.x;
   const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(kDecThreads)
           for (int e = 0; e < 4; ++e) out[k - 3 + e] = (uint8_t)(pack >> (8 * e));
         }
       }
-      model_update(m, CB, blk, sl, wv);  // fk/rangecoder.py:185-186
+      model_update(m, CB, blk, sl, wv, T_add);  // fk/rangecoder.py:185-186
     }
     total += kInc;
     rcp = rcp_next;

@@ -69,6 +69,8 @@ __global__ void __launch_bounds__(rc::kDecThreads)
     rc_encode_kernel(const kvf_rc_stream* __restrict__ streams, int n, int64_t* out_len) {
   using namespace rc;
   extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B, as the decoder's
+  __shared__ uint4 T_add[32];  // in-block increment rows (rc::add_table_init)
+  add_table_init(T_add);       // the whole warp, before any thread leaves
   const int tid = threadIdx.x;
   const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(rc::kDecThreads)
         rng <<= 8;
       }
     }
-    model_update(m, CB, blk, sl, wv);                       // fk/rangecoder.py:133-135
+    model_update(m, CB, blk, sl, wv, T_add);                // fk/rangecoder.py:133-135
     total += kInc;
     rcp = rcp_next;
     if (total >= kLimit) {                                  // fk/rangecoder.py:136-137

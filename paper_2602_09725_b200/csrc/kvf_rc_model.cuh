@@ -90,17 +90,37 @@ __device__ __forceinline__ void model_init(uint4* m, uint32_t (&CB)[16]) {
   for (int k = 0; k < 16; ++k) CB[k] = 16u * k;
 }
 
+// The in-block increments of a symbol at block slot sl, as the 8 packed words
+// added to the block: word w gets INC in its low half if 2w >= sl and in its
+// high half if 2w + 1 >= sl.  A [16 sl][8 w] u32 table in shared memory (one
+// per CTA, 512 B) turns ~48 compare/select instructions per symbol into two
+// 128-bit loads.  Every thread of the (single-warp) CTA writes one uint4.
+__device__ __forceinline__ void add_table_init(uint4* T) {
+  const uint32_t i = threadIdx.x;
+  if (i < 32) {
+    const uint32_t sl = i >> 1, w0 = (i & 1) * 4;
+    uint32_t a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t w = w0 + k;
+      a[k] = (2u * w >= sl ? kInc : 0u) | (2u * w + 1 >= sl ? kInc << 16 : 0u);
+    }
+    T[i] = make_uint4(a[0], a[1], a[2], a[3]);
+  }
+  __syncwarp();
+}
+
 // freq[s] += INC (fk/rangecoder.py:60-66): incl[16 blk + j] += INC for j >= sl
-// (packed 16-bit halves of the block's 8 words `wv`, stored back with two
-// 128-bit stores), CB[k] += INC for k > blk.
+// (packed 16-bit halves of the block's 8 words `wv`, plus the table row of sl,
+// stored back with two 128-bit stores), CB[k] += INC for k > blk.
 __device__ __forceinline__ void model_update(uint4* m, uint32_t (&CB)[16], uint32_t blk,
-                                             uint32_t sl, const uint32_t (&wv)[8]) {
+                                             uint32_t sl, const uint32_t (&wv)[8],
+                                             const uint4* T) {
+  const uint4 a0 = T[2 * sl], a1 = T[2 * sl + 1];
+  const uint32_t add[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
   uint32_t nv[8];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const uint32_t add = (2u * w >= sl ? kInc : 0u) | (2u * w + 1 >= sl ? kInc << 16 : 0u);
-    nv[w] = wv[w] + add;
-  }
+  for (int w = 0; w < 8; ++w) nv[w] = wv[w] + add[w];
   m[(2 * blk) * kDecThreads] = make_uint4(nv[0], nv[1], nv[2], nv[3]);
   m[(2 * blk + 1) * kDecThreads] = make_uint4(nv[4], nv[5], nv[6], nv[7]);
 #pragma unroll
