@@ -468,6 +468,17 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                     finish_batch(inflight.popleft(), clock)
             except Exception as e:  # surfaced on the caller's thread
                 errors.append(e)
+                # Drain to the end marker (every consumer puts it back), so the
+                # receive loop never blocks on a full queue, and let queued GPU
+                # work finish before its buffers can be reused.
+                while work.get() is not None:
+                    pass
+                work.put(None)
+                for b in inflight:
+                    try:
+                        b["done"].synchronize()
+                    except Exception:  # the first error is the one reported
+                        pass
 
     pool_threads = [threading.Thread(target=gpu_worker, args=(k,), daemon=True)
                     for k in range(max(1, workers))]

@@ -213,3 +213,28 @@ def test_pipelined_fetch_batches_k_and_v_into_paged_bf16(tmp_path, monkeypatch, 
             for l in range(5):
                 assert torch.equal(mems[cid].read(t, l), deq[t, l].reshape(-1)), (cid, t, l)
         assert mems[cid].read(0, 5) is None          # pad layer never written
+
+
+@pytest.mark.timeout(300)
+def test_pipelined_fetch_callback_error_propagates(tmp_path):
+    """An exception in on_chunk reaches the caller; the pipeline neither hangs
+    nor leaves the receive loop blocked on a full queue."""
+    cfg = L.identity_layout(8, 32)
+    q, _ = _q(dict(kind="synthetic", T=64, L=3, H=8, D=32, s=0.9, seed=5, c=0.3,
+                   group_size=64, bf16=True))
+    cont = C.pack_chunk(q, cfg, ["R240"], cache_id=b"\x61" * 16, chunk_index=0)
+    payload = cont.bitstream(L.RESOLUTION_CODE["R240"])
+    (tmp_path / C.container_filename(b"\x61" * 16, 0)).write_bytes(cont.to_bytes())
+    meta_store = NS.ChunkStore(str(tmp_path), preload=True)
+    meta, data = meta_store.lookup(b"\x61" * 16, 0, L.RESOLUTION_CODE["R240"])
+
+    def replay(address, cache_id, chunk_index, resolution, timeout_s=30.0, alloc=None):
+        return data, meta, 1e-3
+
+    def boom(rec, res):
+        raise RuntimeError("callback failed")
+
+    chunks = [(b"\x61" * 16, 0)] * 80   # more than the queue depth
+    with pytest.raises(RuntimeError, match="callback failed"):
+        FE.live_fetch_pipeline(None, chunks, None, "fixed:R240", fetch_fn=replay,
+                               on_chunk=boom, depth=4)   # decode-only path (no slot claims)
