@@ -3,10 +3,11 @@
 Keeps the reference's live_fetch_pipeline API and timeline schema
 (fk/netstore.py:367-454, FetchTimeline fk/fetchsim.py:172-205).  The
 reference overlaps one transfer with one CPU decode on a GIL-holding worker
-thread; here a GPU worker owns a CUDA stream: each received payload is
-scanned on the host, copied to the device and entropy-decoded, reconstructed
-and (optionally) restored straight into a PagedMemory block cache, while the
-main thread already receives the next chunk.  Resolution choice is the
+thread; here a GPU worker batches the received payloads: each batch is
+scanned on the host, copied to the device, entropy-decoded, reconstructed
+and (optionally) restored straight into a PagedMemory block cache on its own
+CUDA stream, with several batches in flight, while the main thread keeps
+receiving.  Resolution choice is the
 reference's bubble-minimising rule (fk/fetchsim.py:154-169).
 """
 
@@ -292,10 +293,10 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
     cache holds int8) and on_chunk(record, stats) receives the tokens written.
 
     Receive and GPU work overlap: payloads land in pinned host buffers;
-    ``workers`` GPU worker threads, each with its own CUDA stream, take every
-    chunk received so far (up to ``max_batch``; at most ``depth`` wait) and
-    decode them in ONE codec.decode_batch (a stream's decode is serial, so
-    batching chunks — and running batches concurrently — is what fills the
+    ``workers`` GPU worker threads take every chunk received so far (up to
+    ``max_batch``; at most ``depth`` wait) and decode them in ONE
+    codec.decode_batch (a stream's decode is serial, so batching chunks — and
+    running batches concurrently, each on its own stream — is what fills the
     GPU), then restore them with one batched restore launch.  Chunks write
     disjoint slots, so concurrent batches need no ordering; the host-side slot
     claims are serialised by a lock.
