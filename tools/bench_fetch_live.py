@@ -117,6 +117,24 @@ def check(mems, qs, Lyr, T, n=64):
     return bad
 
 
+def full_check(mems, qs, Lyr, T):
+    """Every (token, layer) slot of every cache against dequantize(): the number
+    of mismatching slots (paged pools gathered through their page maps)."""
+    bad = 0
+    for cid, q in qs.items():
+        mem = mems[cid]
+        tok = torch.arange(T)
+        blk = torch.tensor([mem.pages[int(t) // mem.page_size_tokens] for t in range(0, T, mem.page_size_tokens)])
+        phys = blk[tok // mem.page_size_tokens].cuda()
+        off = (tok % mem.page_size_tokens).cuda()
+        for l in range(Lyr):
+            got = mem.layers[l][phys, off].reshape(T, -1)
+            want = (q.values[:, l].float().reshape(T, q.H * q.D // q.group_size, -1)
+                    * q.scales[l].reshape(1, -1, 1)).reshape(T, -1).to(torch.bfloat16).cuda()
+            bad += int((got != want).any(dim=1).sum())
+    return bad
+
+
 def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
     recs = tl.records
     first = min(r["transfer_start"] for r in recs)
@@ -139,6 +157,7 @@ def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
         "host_restore_s": round(sum(r.get("host_restore_s", 0) for r in {r["decode_start"]: r for r in recs}.values()), 4),
         "gpu_busy_s": round(sum(r["tau_dec"] for r in {r["decode_start"]: r for r in recs}.values()), 4),
         "sampled_slots_mismatch": check(mems, qs, Lyr, args.tokens),
+        "all_slots_mismatch": full_check(mems, qs, Lyr, args.tokens) if args.full_check else None,
         "max_receive_gap_s": round(max((b["transfer_start"] - a["transfer_end"]
                                         for a, b in zip(recs, recs[1:])), default=0.0), 4),
         "max_gap_before_chunk": max(range(1, len(recs)), default=0,
@@ -159,6 +178,7 @@ def main():
     ap.add_argument("--dir", default=None)
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--verbose", action="store_true", help="per-batch timings in each line")
+    ap.add_argument("--full-check", action="store_true", help="compare every slot, not a sample")
     ap.add_argument("--link", default="model", choices=["model", "tcp"],
                     help="model: constant-rate arrival replay; tcp: live loopback server")
     args = ap.parse_args()
