@@ -45,6 +45,34 @@ def test_container_bytes_match_reference(golden):
             assert slab.group_size == q.group_size
 
 
+def test_pack_chunks_batched_equals_pack_chunk(golden):
+    """The batched producer gives byte-identical containers (reference goldens)."""
+    items, cfgs = [], []
+    for c in golden["container"]:
+        q, _ = _q(c["kv"])
+        items.append((c, q))
+    by_cfg = {}
+    for c, q in items:
+        key = (tuple(c["layout"]), tuple(sorted(c["res"])), c["F"])
+        by_cfg.setdefault(key, []).append((c, q))
+    for (lay, res, F), group in by_cfg.items():
+        slabs = [(q, bytes.fromhex(c["cache_id"]), c["chunk_index"], c["token_start"], c["triplet"])
+                 for c, q in group]
+        conts = C.pack_chunks(slabs, L.LayoutConfig(*lay), list(res), F=F)
+        for (c, _), cont in zip(group, conts):
+            assert ref.digest(cont.to_bytes()) == c["bytes"]
+    # many slabs of different lengths in one encode == one at a time
+    q, _ = _q(dict(kind="synthetic", T=150, L=3, H=4, D=8, s=0.9, seed=3, c=0.3, group_size=8))
+    cfg = L.identity_layout(4, 8)
+    slabs = [(KV.QuantizedKV(q.values[t0:t0 + n], q.scales, 8), b"\x07" * 16, k, t0, 0)
+             for k, (t0, n) in enumerate([(0, 64), (64, 50), (114, 36)])]
+    batched = C.pack_chunks(slabs, cfg, ["R240", "R1080"])
+    for s_, cont in zip(slabs, batched):
+        one = C.pack_chunk(s_[0], cfg, ["R240", "R1080"], cache_id=s_[1], chunk_index=s_[2],
+                           token_start=s_[3], layer_triplet_index=s_[4])
+        assert cont.to_bytes() == one.to_bytes()
+
+
 def test_pack_metadata_contents():
     q, _ = _q(dict(kind="synthetic", T=17, L=3, H=4, D=8, s=0.9, seed=0, c=0.0, group_size=8))
     cfg = L.identity_layout(4, 8)
