@@ -197,41 +197,56 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     dev = _dev.device()
     pinned_in = all(isinstance(x, torch.Tensor) for x in streams) and len(streams) > 0
     datas = list(streams) if pinned_in else [_as_bytes(x) for x in streams]
-    idxs = indices if indices is not None else index_streams(datas)
-    if ranges is None:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    # Whole pinned streams with nothing to scan first: their bytes go to the
+    # copy engine at once and the host walk (kvf_kvfc_scan) runs meanwhile.
+    early = pinned_in and indices is None and ranges is None
+    host = None
+    if early:
+        spans = [(0, int(d.numel())) for d in datas]
+        sizes = [hi for _, hi in spans]
+        starts = np.cumsum([0] + sizes)
+        parts = _split_parts(list(range(len(datas))), sizes)
+        blob = _scratch(s, "blob", int(starts[-1]) or 1)
+        side = _enqueue_copies(s, parts, datas, spans, starts, blob, None)
+        idxs = index_streams(datas)
         ranges = [(0, ix.n) for ix in idxs]
+    else:
+        idxs = indices if indices is not None else index_streams(datas)
+        if ranges is None:
+            ranges = [(0, ix.n) for ix in idxs]
     for ix, (f0, f1) in zip(idxs, ranges):
         if not 0 <= f0 <= f1 <= ix.n:
             raise ValueError("frame range outside the stream")
         if f0 < f1 and ix.frame_type[f0] != 0:
             raise ValueError("a partial decode must start at an intra frame")
-    # Only the byte span of the decoded frames travels to the device.
-    spans = []
-    for ix, (f0, f1) in zip(idxs, ranges):
-        if f1 <= f0:
-            spans.append((0, 0))
-            continue
-        ks = slice(3 * f0, 3 * f1)
-        heads = np.where(ix.bitmap_off[ks] >= 0, ix.bitmap_off[ks], ix.payload_off[ks])
-        spans.append((int(heads.min()),
-                      int((ix.payload_off[ks] + ix.payload_len[ks]).max())))
-    sizes = [hi - lo for lo, hi in spans]
-    starts = np.cumsum([0] + sizes)
-    s = stream if stream is not None else torch.cuda.current_stream()
     live = [j for j, (f0, f1) in enumerate(ranges) if f1 > f0]
-    parts = _split_parts(live, [sizes[j] for j in live])
-    host = None
-    if not pinned_in:
-        host = _STAGING.acquire(int(starts[-1]) or 1)
-        hv = host.numpy()
-        for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
-            hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
+    if not early:
+        # Only the byte span of the decoded frames travels to the device.
+        spans = []
+        for ix, (f0, f1) in zip(idxs, ranges):
+            if f1 <= f0:
+                spans.append((0, 0))
+                continue
+            ks = slice(3 * f0, 3 * f1)
+            heads = np.where(ix.bitmap_off[ks] >= 0, ix.bitmap_off[ks], ix.payload_off[ks])
+            spans.append((int(heads.min()),
+                          int((ix.payload_off[ks] + ix.payload_len[ks]).max())))
+        sizes = [hi - lo for lo, hi in spans]
+        starts = np.cumsum([0] + sizes)
+        parts = _split_parts(live, [sizes[j] for j in live])
+        if not pinned_in:
+            host = _STAGING.acquire(int(starts[-1]) or 1)
+            hv = host.numpy()
+            for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
+                hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
+        blob = _scratch(s, "blob", int(starts[-1]) or 1)
+        side = _enqueue_copies(s, parts, datas, spans, starts, blob, host)
     hw_all = np.array([ix.h * ix.w for ix in idxs], np.int64)
     hw16_all = -(-hw_all // 16) * 16                 # 16-byte aligned symbol slots
     nf_all = np.array([f1 - f0 for f0, f1 in ranges], np.int64)
     sym_at = np.concatenate([[0], np.cumsum(3 * nf_all * hw16_all)])
     frames = []
-    blob = _scratch(s, "blob", int(starts[-1]) or 1)
     symbols = _scratch(s, "symbols", max(int(sym_at[-1]), 1))
     with torch.cuda.stream(s):
         for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
@@ -240,29 +255,24 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
             if tuple(fr.shape) != (f1 - f0, 3, ix.h, ix.w):
                 raise ValueError("output frames have the wrong shape")
             frames.append(fr)
-    # Parts are pipelined on side streams: part p's two kernels follow its
-    # coded bytes on its stream, so they overlap the copies of parts p+1..
-    # (Every side stream first waits for the work `s` had before this call,
-    # so the memory allocated above on `s` is free.)
-    side = _side_streams(s, len(parts)) if len(parts) > 1 else [s]
-    for t in side:
-        if t is not s:
-            t.wait_stream(s)
-    # every part's coded bytes go on the copy engine first ...
-    for p, part in enumerate(parts):
-        with torch.cuda.stream(side[p]):
-            for j in part:
-                lo, hi = spans[j]
-                s0 = int(starts[j])
-                src = datas[j][lo:hi] if pinned_in else host[s0:s0 + hi - lo]
-                blob[s0:s0 + hi - lo].copy_(src, non_blocking=True)
-    # ... then, part by part, the descriptors are built on the host while
-    # those copies run, and the kernels read them in place from pinned host
-    # memory (mapped, UVA): no H2D copy of their own to queue behind the bytes
+    # Part by part, the descriptors are built on the host while the copies
+    # run; part p's two kernels follow its coded bytes on its stream, so they
+    # overlap the copies of parts p+1..  The kernels read the descriptors in
+    # place from pinned host memory (mapped, UVA): no H2D copy of their own
+    # queues behind the bytes.  (The side streams waited for all work `s` had
+    # when they were set up, and nothing was queued on `s` since, so `symbols`
+    # and `frames`, allocated on `s` afterwards, are free for them.)
     base = blob.data_ptr()
     done, keep = [], []
     for p, part in enumerate(parts):
         t = side[p]
+        part = [j for j in part if ranges[j][1] > ranges[j][0]]
+        if not part:
+            if t is not s:
+                ev = torch.cuda.Event()
+                ev.record(t)
+                done.append((t, ev))
+            continue
         rc, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, base,
                                              symbols.data_ptr() + sym_at, frames)
         h_rc, h_planes, h_chains = (_pinned_copy(x) for x in (rc, flat, ch_arr))
@@ -291,6 +301,25 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
         for u, _ in done:
             t.record_stream(u)
     return frames, held
+
+
+def _enqueue_copies(s, parts, datas, spans, starts, blob, host):
+    """Queue each part's H2D copies on its side stream (after the work `s` has
+    so far); returns the side streams (just [s] for a single part)."""
+    side = _side_streams(s, len(parts)) if len(parts) > 1 else [s]
+    for t in side:
+        if t is not s:
+            t.wait_stream(s)
+    for p, part in enumerate(parts):
+        with torch.cuda.stream(side[p]):
+            for j in part:
+                lo, hi = spans[j]
+                if hi <= lo:
+                    continue
+                s0 = int(starts[j])
+                src = datas[j][lo:hi] if host is None else host[s0:s0 + hi - lo]
+                blob[s0:s0 + hi - lo].copy_(src, non_blocking=True)
+    return side
 
 
 _SCRATCH = collections.OrderedDict()   # (device, stream, name) -> grow-only device buffer
