@@ -179,16 +179,21 @@ _STAGING = _PinnedStaging()
 _OUT_STAGING = _PinnedStaging()   # encode_batch's D2H of the coded streams
 
 
-def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
+def decode_batch(streams, out=None, stream=None, ranges=None, indices=None,
+                 max_parts=None):
     """Decode many KVFC streams on the GPU: two launches (range decode,
     reconstruction) per part of up to _MAX_PARTS, pipelined with the H2D copy.
 
     ``streams``: list of bytes / Bitstream (staged through a reused pinned
     buffer), or of contiguous CPU uint8 tensors — pinned receive buffers —
     which are copied to the device directly.  ``out``: optional list of
-    [n, 3, h, w] uint8 CUDA tensors (any row pitch) to decode into.
+    [n, 3, h, w] uint8 CUDA tensors (any row pitch) to decode into, or a
+    callable taking the list of those shapes (known after the stream walk)
+    and returning the tensors.
     ``ranges``: optional per-stream (first, stop) frame range; ``first`` must
     be an intra frame (a chain start), and the output holds stop-first frames.
+    ``max_parts`` caps the part pipeline (default _MAX_PARTS; each part runs on
+    its own side stream of ``stream``).
     Returns (frames list, device bytes held).  Raises DecodeError like the
     reference.  The work is ordered on ``stream`` (default: current): callers
     see the frames after it.  Calls on one stream must come from one thread
@@ -206,7 +211,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
         spans = [(0, int(d.numel())) for d in datas]
         sizes = [hi for _, hi in spans]
         starts = np.cumsum([0] + sizes)
-        parts = _split_parts(list(range(len(datas))), sizes)
+        parts = _split_parts(list(range(len(datas))), sizes, max_parts)
         blob = _scratch(s, "blob", int(starts[-1]) or 1)
         side = _enqueue_copies(s, parts, datas, spans, starts, blob, None)
         idxs = index_streams(datas)
@@ -234,7 +239,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
                           int((ix.payload_off[ks] + ix.payload_len[ks]).max())))
         sizes = [hi - lo for lo, hi in spans]
         starts = np.cumsum([0] + sizes)
-        parts = _split_parts(live, [sizes[j] for j in live])
+        parts = _split_parts(live, [sizes[j] for j in live], max_parts)
         if not pinned_in:
             host = _STAGING.acquire(int(starts[-1]) or 1)
             hv = host.numpy()
@@ -248,6 +253,9 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None):
     sym_at = np.concatenate([[0], np.cumsum(3 * nf_all * hw16_all)])
     frames = []
     symbols = _scratch(s, "symbols", max(int(sym_at[-1]), 1))
+    if callable(out):
+        with torch.cuda.stream(s):
+            out = out([(f1 - f0, 3, ix.h, ix.w) for ix, (f0, f1) in zip(idxs, ranges)])
     with torch.cuda.stream(s):
         for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
             fr = out[j] if out is not None else torch.empty((f1 - f0, 3, ix.h, ix.w),
@@ -461,11 +469,11 @@ _MAX_PARTS = 8
 _SIDE = {}
 
 
-def _split_parts(idx, sizes):
+def _split_parts(idx, sizes, max_parts=None):
     """Consecutive groups of `idx` with about equal bytes: one group below
-    _PART_BYTES, else up to _MAX_PARTS."""
+    _PART_BYTES, else up to `max_parts` (default _MAX_PARTS)."""
     total = sum(sizes)
-    n = min(_MAX_PARTS, len(idx), max(1, total // _PART_BYTES))
+    n = min(max_parts or _MAX_PARTS, len(idx), max(1, total // _PART_BYTES))
     if n <= 1:
         return [list(idx)]
     parts, cur, acc, target = [], [], 0, total / n

@@ -156,3 +156,14 @@ def test_part_pipeline_many_parts(monkeypatch, pinned):
     for fr, (a, b), o in zip(frames, ranges, out):
         assert tuple(o.shape) == (b - a,) + fr.shape[1:]
         assert np.array_equal(o.cpu().numpy(), fr[a:b])
+    # whole streams (copied before the host walk), a callable `out`, capped parts
+    seen = []
+
+    def alloc(shapes):
+        seen.extend(shapes)
+        return [torch.zeros(shp, dtype=torch.uint8, device="cuda") for shp in shapes]
+
+    out2, _ = codec.decode_batch(streams, out=alloc, max_parts=3)
+    assert seen == [fr.shape for fr in frames]
+    for fr, o in zip(frames, out2):
+        assert np.array_equal(o.cpu().numpy(), fr)
