@@ -190,6 +190,14 @@ kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan,
 kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
                           void* stream);
 
+/* Phase 2 only, for up to n_units units whose `absmax` the caller already
+ * filled with the per-(plane, group) maxima of the same source (e.g. a KV
+ * writer that tracks them as it stores K/V, or an earlier kvf_pack_absmax):
+ * scales + frames in a single read of the source.  Samples beyond a supplied
+ * maximum are clipped exactly as the reference clips (fk/kvmodel.py:142). */
+kvf_status kvf_pack_frames_batch(const kvf_pack_unit* units, int32_t n_units,
+                                 void* stream);
+
 /* u32 words of pack scratch a unit of this plan needs: 6*G (G = H*D/group_size). */
 int64_t kvf_pack_scratch_words(const kvf_plan* plan);
 

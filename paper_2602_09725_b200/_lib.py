@@ -145,6 +145,7 @@ _SIGNATURES = {
     "kvf_pack_frames": (C.c_int, [C.POINTER(kvf_paged), C.POINTER(kvf_plan), _VP, _VP,
                                   C.POINTER(kvf_surface), _VP]),
     "kvf_pack_batch": (C.c_int, [C.POINTER(kvf_pack_unit), C.c_int32, _VP]),
+    "kvf_pack_frames_batch": (C.c_int, [C.POINTER(kvf_pack_unit), C.c_int32, _VP]),
     "kvf_pack_scratch_words": (C.c_int64, [C.POINTER(kvf_plan)]),
     "kvf_quantize": (C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                _VP, _VP, _VP, _VP]),

@@ -506,6 +506,11 @@ extern "C" kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units
   return run(units, n_units, 1 | 2 | 4 | 8, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" kvf_status kvf_pack_frames_batch(const kvf_pack_unit* units, int32_t n_units,
+                                            void* stream) {
+  return run(units, n_units, 4 | 8, reinterpret_cast<cudaStream_t>(stream));
+}
+
 extern "C" kvf_status kvf_pack_absmax(const kvf_paged* src, const kvf_plan* plan,
                                       uint32_t* absmax, void* stream) {
   if (!src || !plan || !absmax) KVF_FAIL(KVF_EINVAL, "null argument");

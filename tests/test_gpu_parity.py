@@ -498,3 +498,40 @@ def test_tiny_and_ragged_units_pack_then_restore(mode, monkeypatch):
     for (T, lay, plan, v, s, want, fr, sc), out in zip(checks, outs):
         got = torch.stack([o.cpu() for o in out], 1).numpy().reshape(T, 3, -1)
         assert np.array_equal(got, v.reshape(T, 3, -1)), (T, lay)
+
+
+def test_pack_frames_batch_with_supplied_maxima():
+    """kvf_pack_frames_batch (scales + frames from caller-supplied maxima, one
+    read of the source) equals the oracle, and clips like the reference when a
+    supplied maximum is smaller than the data."""
+    lay = (8, 128, 1, 8, 1, 128)
+    H, D, res, gs = 8, 128, "R240", 128
+    T = 333
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, 3, H, D, 0.9, 21, 0.3))
+    kv = np_bf16_from_f32(x).cuda()
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+    v, s = ref.quantize(x, gs)
+    want = ref.assemble_frames(v.reshape(T, 3, H * D), ref.Plan(T, res, *lay, F=4))
+    # maxima as f32 bit patterns, as kvf_pack_absmax leaves them
+    mx = np.abs(x.reshape(T, 3, H * D // gs, gs)).max(axis=(0, 3)).astype(np.float32)
+    for shrink in (1.0, 0.5):
+        am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)), dtype=torch.int32)
+        am[:mx.size] = torch.from_numpy((mx * np.float32(shrink)).view(np.int32).reshape(-1))
+        am = am.cuda()
+        fr = torch.empty(plan.frame_shape(), dtype=torch.uint8, device="cuda")
+        sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
+        u, _ = _pack_unit(kv, lay, res, 0, T, 4, gs, fr, am, sc)
+        _lib.call("kvf_pack_frames_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
+        torch.cuda.synchronize()
+        if shrink == 1.0:
+            assert np.array_equal(sc.cpu().numpy(), s)
+            assert np.array_equal(fr.cpu().numpy(), want)
+        else:   # reference arithmetic with the smaller scale: clip to +-127
+            s2 = np.where(mx * np.float32(shrink) > 0,
+                          (np.float64(mx * np.float32(shrink)) / 127.0).astype(np.float32), 1.0)
+            q = np.clip(np.rint(x.reshape(T, 3, H * D // gs, gs).astype(np.float64)
+                                / s2[None, :, :, None].astype(np.float64)), -127, 127)
+            want2 = ref.assemble_frames(q.astype(np.int8).reshape(T, 3, H * D),
+                                        ref.Plan(T, res, *lay, F=4))
+            assert np.array_equal(sc.cpu().numpy(), s2)
+            assert np.array_equal(fr.cpu().numpy(), want2)
