@@ -91,15 +91,15 @@ struct ByteWindow {
 __global__ void __launch_bounds__(kDecThreads)
     rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n) {
   extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B
-  __shared__ uint4 T_add[32];  // in-block increment rows (rc::add_table_init)
+  __shared__ uint4 T_add[2 * kAddRows];  // increment rows (rc::add_table_init)
   add_table_init(T_add);       // the whole warp, before any thread leaves
   const int tid = threadIdx.x;
   const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
   const kvf_rc_stream st = streams[sidx];
   uint4* m = M + tid;  // chunk c of this thread's model at m[c * kDecThreads]
-  uint32_t CB[16];
-  model_init(m, CB);
+  uint32_t P[8];       // block prefixes CB[2w] | CB[2w+1] << 16
+  model_init(m, P);
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu, code = 0;
   ByteWindow bw;
   bw.init(st.payload, (uint32_t)st.len);
@@ -126,23 +126,25 @@ __global__ void __launch_bounds__(kDecThreads)
     // The level-i operand is CB[(bits above) | 2^i]; CB[blk] is the operand of
     // the last level that compared true (CB[0] = 0 if none), so `base` is a
     // 4-select chain that finishes one select after b0.
-    const uint32_t o3 = CB[8];
+    // (CB[2w] is the low and CB[2w+1] the high half of P[w]; the selects pick
+    // packed words, levels 3..1 read low halves, level 0 a high half)
+    const uint32_t o3 = cb_lo(P[4]);                               // CB[8]
     const bool b3 = o3 * r <= x;
-    const uint32_t o2 = b3 ? CB[12] : CB[4];
+    const uint32_t o2 = cb_lo(b3 ? P[6] : P[2]);                   // CB[12] : CB[4]
     const bool b2 = o2 * r <= x;
-    const uint32_t c2a = b3 ? CB[10] : CB[2], c2b = b3 ? CB[14] : CB[6];
-    const uint32_t o1 = b2 ? c2b : c2a;
+    const uint32_t w2a = b3 ? P[5] : P[1], w2b = b3 ? P[7] : P[3];  // CB[10|2], CB[14|6]
+    const uint32_t o1 = cb_lo(b2 ? w2b : w2a);
     const bool b1 = o1 * r <= x;
-    const uint32_t c1a = b3 ? CB[9] : CB[1], c1b = b3 ? CB[11] : CB[3];
-    const uint32_t c1c = b3 ? CB[13] : CB[5], c1d = b3 ? CB[15] : CB[7];
-    const uint32_t c1e = b2 ? c1c : c1a, c1f = b2 ? c1d : c1b;
-    const uint32_t o0 = b1 ? c1f : c1e;
+    const uint32_t w1a = b3 ? P[4] : P[0], w1c = b3 ? P[6] : P[2];  // CB[9|1], CB[13|5]
+    const uint32_t w1e = b2 ? w1c : w1a, w1f = b2 ? w2b : w2a;       // (+ CB[11|3|15|7])
+    const uint32_t o0 = cb_hi(b1 ? w1f : w1e);
     const bool b0 = o0 * r <= x;
     const uint32_t blk = (b3 ? 8u : 0u) + (b2 ? 4u : 0u) + (b1 ? 2u : 0u) + (b0 ? 1u : 0u);
     uint32_t base = b3 ? o3 : 0u;
     base = b2 ? o2 : base;
     base = b1 ? o1 : base;
     base = b0 ? o0 : base;
+    const uint4 cbi[2] = {T_add[2 * (blk + 1)], T_add[2 * (blk + 1) + 1]};  // CB[q>blk] += INC
     const uint32_t rem = x - base * r;
     // within the block: incl[0..15] from two 128-bit loads
     const uint4 ca = m[(2 * blk) * kDecThreads], cb = m[(2 * blk + 1) * kDecThreads];
@@ -210,12 +212,12 @@ __global__ void __launch_bounds__(kDecThreads)
           for (int e = 0; e < 4; ++e) out[k - 3 + e] = (uint8_t)(pack >> (8 * e));
         }
       }
-      model_update(m, CB, blk, sl, wv, T_add);  // fk/rangecoder.py:185-186
+      model_update(m, P, blk, sl, wv, T_add, cbi);  // fk/rangecoder.py:185-186
     }
     total += kInc;
     rcp = rcp_next;
     if (total >= kLimit) {
-      total = rebuild(m, CB);
+      total = rebuild(m, P);
       rcp = rcp_approx(total);
     }
   }

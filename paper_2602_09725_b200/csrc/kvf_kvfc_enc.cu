@@ -69,15 +69,15 @@ __global__ void __launch_bounds__(rc::kDecThreads)
     rc_encode_kernel(const kvf_rc_stream* __restrict__ streams, int n, int64_t* out_len) {
   using namespace rc;
   extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B, as the decoder's
-  __shared__ uint4 T_add[32];  // in-block increment rows (rc::add_table_init)
+  __shared__ uint4 T_add[2 * kAddRows];  // increment rows (rc::add_table_init)
   add_table_init(T_add);       // the whole warp, before any thread leaves
   const int tid = threadIdx.x;
   const int sidx = blockIdx.x * kDecThreads + tid;
   if (sidx >= n) return;
   const kvf_rc_stream st = streams[sidx];
   uint4* m = M + tid;
-  uint32_t CB[16];
-  model_init(m, CB);
+  uint32_t P[8];  // block prefixes CB[2w] | CB[2w+1] << 16
+  model_init(m, P);
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu;
   uint8_t* out = const_cast<uint8_t*>(st.payload);
   const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
@@ -114,19 +114,19 @@ __global__ void __launch_bounds__(rc::kDecThreads)
     const uint32_t j1 = sl - 1;  // wraps for sl == 0 (value unused then)
     const uint32_t lo_raw = m16[((2 * blk + ((j1 >> 3) & 1)) * kDecThreads) * 8 + (j1 & 7)];
     const uint32_t lo_v = sl == 0 ? 0u : lo_raw;
-    // CB[blk] by a 4-level select tree on the bits of blk
+    // CB[blk]: a 3-level select tree picks the packed word P[blk >> 1], the
+    // low bit of blk its half
     uint32_t base;
     {
-      const bool k3 = blk & 8, k2 = blk & 4, k1 = blk & 2, k0 = blk & 1;
-      uint32_t e[8];
+      const bool k3 = blk & 8, k2 = blk & 4, k1 = blk & 2;
+      uint32_t e[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) e[i] = k3 ? CB[8 + i] : CB[i];
-      uint32_t f4[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) f4[i] = k2 ? e[4 + i] : e[i];
-      const uint32_t g0 = k1 ? f4[2] : f4[0], g1 = k1 ? f4[3] : f4[1];
-      base = k0 ? g1 : g0;
+      for (int i = 0; i < 4; ++i) e[i] = k3 ? P[4 + i] : P[i];
+      const uint32_t f0 = k2 ? e[2] : e[0], f1 = k2 ? e[3] : e[1];
+      const uint32_t w = k1 ? f1 : f0;
+      base = (blk & 1) ? cb_hi(w) : cb_lo(w);
     }
+    const uint4 cbi[2] = {T_add[2 * (blk + 1)], T_add[2 * (blk + 1) + 1]};
     const uint32_t cum = base + lo_v, fr = hi_v - lo_v;     // fk/rangecoder.py:114-115
     const uint32_t r = exact_div(rng, total, rcp);          // fk/rangecoder.py:117
     low += r * cum;
@@ -145,11 +145,11 @@ __global__ void __launch_bounds__(rc::kDecThreads)
         rng <<= 8;
       }
     }
-    model_update(m, CB, blk, sl, wv, T_add);                // fk/rangecoder.py:133-135
+    model_update(m, P, blk, sl, wv, T_add, cbi);            // fk/rangecoder.py:133-135
     total += kInc;
     rcp = rcp_next;
     if (total >= kLimit) {                                  // fk/rangecoder.py:136-137
-      total = rebuild(m, CB);
+      total = rebuild(m, P);
       rcp = rcp_approx(total);
     }
   }

@@ -36,7 +36,7 @@ __device__ __forceinline__ uint32_t hi16(uint32_t w) { return w >> 16; }
 
 // Halve every count ((f + 1) >> 1, fk/rangecoder.py:93-103) and rebuild the
 // cumulative arrays; returns the new total.
-__device__ __forceinline__ uint32_t rebuild(uint4* m, uint32_t (&CB)[16]) {
+__device__ __forceinline__ uint32_t rebuild(uint4* m, uint32_t (&P)[8]) {
   uint32_t total = 0;
 #pragma unroll 1
   for (int b = 0; b < 16; ++b) {
@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t rebuild(uint4* m, uint32_t (&CB)[16]) {
   uint32_t run = 0;
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
-    CB[b] = run;
+    if (b & 1) P[b >> 1] |= run << 16; else P[b >> 1] = run;
     const uint4 c1 = m[(2 * b + 1) * kDecThreads];
     run += hi16(c1.w);
   }
@@ -78,8 +78,8 @@ __device__ __forceinline__ uint32_t exact_div(uint32_t rng, uint32_t total, floa
   return q0 + (uint32_t)d + (rem1 >= (int32_t)total ? 1u : 0u) - (rem1 < 0 ? 1u : 0u);
 }
 
-// counts start at 1: incl[16b + j] = j + 1, CB[k] = 16k
-__device__ __forceinline__ void model_init(uint4* m, uint32_t (&CB)[16]) {
+// counts start at 1: incl[16b + j] = j + 1, CB[k] = 16k (packed: P[w] = CB[2w] | CB[2w+1] << 16)
+__device__ __forceinline__ void model_init(uint4* m, uint32_t (&P)[8]) {
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const uint32_t j0 = (c & 1) * 8 + 1;
@@ -87,35 +87,40 @@ __device__ __forceinline__ void model_init(uint4* m, uint32_t (&CB)[16]) {
                                     (j0 + 4) | (j0 + 5) << 16, (j0 + 6) | (j0 + 7) << 16);
   }
 #pragma unroll
-  for (int k = 0; k < 16; ++k) CB[k] = 16u * k;
+  for (int w = 0; w < 8; ++w) P[w] = (32u * w) | ((32u * w + 16u) << 16);
 }
 
-// The in-block increments of a symbol at block slot sl, as the 8 packed words
-// added to the block: word w gets INC in its low half if 2w >= sl and in its
-// high half if 2w + 1 >= sl.  A [16 sl][8 w] u32 table in shared memory (one
-// per CTA, 512 B) turns ~48 compare/select instructions per symbol into two
-// 128-bit loads.  Every thread of the (single-warp) CTA writes one uint4.
+// Increment rows: row t (t = 0..16) is 8 packed words, word w holding INC in
+// its low half if 2w >= t and in its high half if 2w + 1 >= t.  Row sl is
+// what a symbol at block slot sl adds to its block's inclusive sums; row
+// blk + 1 is what it adds to the packed block prefixes (CB[q] for q > blk).
+// One table per CTA in shared memory (544 B); the kernels load row blk + 1 as
+// soon as blk is known, so the load is off the next symbol's search chain.
+constexpr int kAddRows = 17;
 __device__ __forceinline__ void add_table_init(uint4* T) {
-  const uint32_t i = threadIdx.x;
-  if (i < 32) {
-    const uint32_t sl = i >> 1, w0 = (i & 1) * 4;
+  for (uint32_t i = threadIdx.x; i < 2 * kAddRows; i += 32) {
+    const uint32_t t = i >> 1, w0 = (i & 1) * 4;
     uint32_t a[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t w = w0 + k;
-      a[k] = (2u * w >= sl ? kInc : 0u) | (2u * w + 1 >= sl ? kInc << 16 : 0u);
+      a[k] = (2u * w >= t ? kInc : 0u) | (2u * w + 1 >= t ? kInc << 16 : 0u);
     }
     T[i] = make_uint4(a[0], a[1], a[2], a[3]);
   }
   __syncwarp();
 }
 
+__device__ __forceinline__ uint32_t cb_lo(uint32_t w) { return w & 0xFFFFu; }
+__device__ __forceinline__ uint32_t cb_hi(uint32_t w) { return w >> 16; }
+
 // freq[s] += INC (fk/rangecoder.py:60-66): incl[16 blk + j] += INC for j >= sl
-// (packed 16-bit halves of the block's 8 words `wv`, plus the table row of sl,
-// stored back with two 128-bit stores), CB[k] += INC for k > blk.
-__device__ __forceinline__ void model_update(uint4* m, uint32_t (&CB)[16], uint32_t blk,
+// (the block's 8 packed words `wv` plus table row sl, two 128-bit stores) and
+// CB[q] += INC for q > blk (the packed prefixes plus row blk + 1, `cbi`,
+// loaded by the caller as soon as blk was known).
+__device__ __forceinline__ void model_update(uint4* m, uint32_t (&P)[8], uint32_t blk,
                                              uint32_t sl, const uint32_t (&wv)[8],
-                                             const uint4* T) {
+                                             const uint4* T, const uint4 (&cbi)[2]) {
   const uint4 a0 = T[2 * sl], a1 = T[2 * sl + 1];
   const uint32_t add[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
   uint32_t nv[8];
@@ -123,9 +128,8 @@ __device__ __forceinline__ void model_update(uint4* m, uint32_t (&CB)[16], uint3
   for (int w = 0; w < 8; ++w) nv[w] = wv[w] + add[w];
   m[(2 * blk) * kDecThreads] = make_uint4(nv[0], nv[1], nv[2], nv[3]);
   m[(2 * blk + 1) * kDecThreads] = make_uint4(nv[4], nv[5], nv[6], nv[7]);
-#pragma unroll
-  for (int q = 1; q < 16; ++q)
-    if ((uint32_t)q > blk) CB[q] += kInc;
+  P[0] += cbi[0].x; P[1] += cbi[0].y; P[2] += cbi[0].z; P[3] += cbi[0].w;
+  P[4] += cbi[1].x; P[5] += cbi[1].y; P[6] += cbi[1].z; P[7] += cbi[1].w;
 }
 
 }  // namespace rc
