@@ -191,7 +191,7 @@ class Workload:
         self.all_units = len(all_units)
         self.mine = shard.units_for_rank(all_units, rank, world, args.shard, H, D)
         self.pack_units, self.units, self.frames, self.scales = [], [], [], []
-        self.caches, self._keep, self._specs = [], [], []
+        self.caches, self._keep, self._specs, self.slabs = [], [], [], []
         self.elems = sum(u.elements(H, D) for u in self.mine)
         keys = sorted({(u.request, u.kv, u.triplet) for u in self.mine})
         for (r, kv_i, j) in keys:
@@ -201,6 +201,7 @@ class Workload:
                                        dtype=torch.bfloat16).data
             cache = torch.empty((real, nblk + 64, bs, H, D), dtype=torch.bfloat16, device=device)
             self._keep += [slab]
+            self.slabs.append(slab)
             self.caches.append(cache)
             for u in (u for u in self.mine if (u.request, u.kv, u.triplet) == (r, kv_i, j)):
                 t0, tc = u.token_start, u.tokens
@@ -245,6 +246,31 @@ class Workload:
         self._lib, self._dev, self._L = _lib, _dev, L
         self.n_launch_restore = (len(self.units) + _lib.KVF_MAX_UNITS - 1) // _lib.KVF_MAX_UNITS
         self.n_launch_pack = 4 * self.n_launch_restore
+
+    def check_restored(self, per_unit=16):
+        """Sampled slots of the restored caches against an independent path:
+        the whole-tensor quantize kernel (kvf_quantize) of each unit's token
+        chunk, dequantised in fp32 and rounded to bf16.  Returns (slots, mismatches)."""
+        torch = self.torch
+        from paper_2602_09725_b200 import kvmodel as KV
+        g = torch.Generator(device="cpu")
+        g.manual_seed(7)
+        slots = bad = 0
+        keys = sorted({(u.request, u.kv, u.triplet) for u in self.mine})
+        for (r, kv_i, j), slab, cache in zip(keys, self.slabs, self.caches):
+            for u in (u for u in self.mine if (u.request, u.kv, u.triplet) == (r, kv_i, j)):
+                t0, tc = u.token_start, u.tokens
+                q = KV.quantize(KV.KVCache(slab[t0:t0 + tc].contiguous()), self.gs)
+                deq = KV.dequantize(q, torch.bfloat16).data          # [tc, real, H, D]
+                toks = torch.randint(0, tc, (per_unit,), generator=g)
+                for t in toks.tolist():
+                    tt = t0 + t
+                    blk = int(self.table[tt // self.page])
+                    for p in range(u.real_layers):
+                        got = cache[p][blk, tt % self.page]
+                        slots += 1
+                        bad += int(not torch.equal(got, deq[t, p]))
+        return slots, bad
 
     def frames_at(self, res):
         """Pack every unit again at another resolution class (same sources,
@@ -532,6 +558,7 @@ def main():
     achieved = 3.0 * w.elems / (ms * 1e-3) / 1e9  # per GPU, algorithmic bytes
     pack_ach = 3.0 * w.elems / (pack_ms * 1e-3) / 1e9
 
+    chk_slots, chk_bad = w.check_restored()   # after the timed restores, outside timing
     e2e = None
     if not args.no_e2e:
         e2e_ms, h2d, d2h = e2e_restore(w, max(3, args.steps // 4), torch)
@@ -593,6 +620,9 @@ def main():
             "e2e": e2e,
             "fetch_to_ready": fetch,
             "gpu_launches": w.n_launch_restore * args.steps,
+            "restore_check": {"slots": chk_slots, "mismatch": chk_bad,
+                              "against": "kvf_quantize of each unit's token chunk, "
+                                         "dequantised and rounded to bf16 (sampled slots)"},
             "clocks": clocks,
             "pack": {"ms_per_step": round(pack_ms, 4),
                      "achieved_gbs": round(pack_ach, 1), "frac": round(pack_ach / peak, 4),
