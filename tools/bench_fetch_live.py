@@ -242,7 +242,7 @@ def main():
                 stop.set()
                 srv.join(timeout=30)
             emit(tl, res, rate or None, coded, mems, qs, Lyr, args, setup_s,
-                 "loopback TCP, reference wire protocol, token-bucket egress")
+                 "loopback TCP, reference wire protocol, paced egress")
             del mems
     if args.dir is None:
         shutil.rmtree(root, ignore_errors=True)
