@@ -6,7 +6,8 @@ loopback link (BASELINE.json configs[4]), GPU decode + restore into paged bf16.
 Packs the context into the reference's containers (88 units: K/V x 11 layer
 triplets x 4 chunks of <= 10,000 tokens; scales over all tokens, as
 fk/cli.py:222-224), writes them to a ChunkStore directory, serves it with the
-reference wire protocol and a token-bucket egress limit (fk/netstore.py:188-211),
+reference wire protocol and an egress pacer at the link rate (the reference throttles with
+a token bucket, fk/netstore.py:188-211),
 and runs live_fetch_pipeline into two PagedMemory caches (K and V).  Prints one
 JSON line per (resolution, rate): time to ready (first request -> last restore
 complete), the link time the coded bytes need at that rate, the rate the
