@@ -73,6 +73,21 @@ def test_pack_chunks_batched_equals_pack_chunk(golden):
         assert cont.to_bytes() == one.to_bytes()
 
 
+def test_unpack_chunks_batched_equals_unpack_chunk(golden):
+    conts = []
+    for c in golden["container"]:
+        q, _ = _q(c["kv"])
+        cont = C.pack_chunk(q, L.LayoutConfig(*c["layout"]), c["res"],
+                            cache_id=bytes.fromhex(c["cache_id"]), chunk_index=c["chunk_index"],
+                            token_start=c["token_start"], layer_triplet_index=c["triplet"],
+                            F=c["F"])
+        conts += [(cont, code, q) for code in cont.resolutions]
+    batched = C.unpack_chunks([(cont, code) for cont, code, _ in conts])
+    for (cont, code, q), slab in zip(conts, batched):
+        assert torch.equal(slab.values, q.values) and torch.equal(slab.scales, q.scales)
+        assert slab.group_size == q.group_size
+
+
 def test_pack_metadata_contents():
     q, _ = _q(dict(kind="synthetic", T=17, L=3, H=4, D=8, s=0.9, seed=0, c=0.0, group_size=8))
     cfg = L.identity_layout(4, 8)
