@@ -238,8 +238,12 @@ void launch_fast(int vpl, const RestoreParams& P, dim3 grid, cudaStream_t s) {
 // Launch one group of units that share (variant, dtype).
 kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
                         int32_t dtype, cudaStream_t s) {
-  for (size_t at = 0; at < units.size(); at += KVF_MAX_UNITS) {
-    size_t n = std::min<size_t>(KVF_MAX_UNITS, units.size() - at);
+  // equal launches (e.g. 280 units: 94 + 93 + 93, not 128 + 128 + 24, whose
+  // last small launch would leave most SMs idle)
+  const size_t n_launch = (units.size() + KVF_MAX_UNITS - 1) / KVF_MAX_UNITS;
+  const size_t per = n_launch ? (units.size() + n_launch - 1) / n_launch : 0;
+  for (size_t at = 0; at < units.size(); at += per) {
+    size_t n = std::min<size_t>(per, units.size() - at);
     RestoreParams P;
     P.n_units = (int32_t)n;
     int64_t max_work = 0;
