@@ -223,7 +223,7 @@ def main():
             mems = new_mems(qs, args.tokens, Lyr, H, D)
             gc.collect()   # no collector pause inside the timed fetch
             torch.cuda.synchronize()
-            tl = FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=rate, mem=mems,
+            tl = FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=rate or 400.0, mem=mems,
                                         real_layers=Lyr, fetch_fn=link, workers=args.workers)
             emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, "modelled constant-rate link")
             del mems, link
