@@ -149,3 +149,47 @@ def test_b200_lookup_table_and_adaptive_choice():
     assert FE.select_resolution(100.0, 1, "R1080", t) == "R240"
     assert FE.select_resolution(10.0, 1, "R1080", t) == "R240"
     assert FE.select_resolution(1.0, 1, "R1080", t) == "R1080"
+
+
+def test_pacer_holds_the_link_rate():
+    """The server's egress pacer (netstore._Pacer) sends at the configured rate."""
+    import time
+    p = NS._Pacer(8.0)                       # 1 GB/s
+    t0 = time.monotonic()
+    sent = 0
+    while sent < 100_000_000:
+        p.wait(p.slice)
+        sent += p.slice
+    dt = time.monotonic() - t0
+    assert 0.08 <= dt <= 0.25, dt             # 0.1 s less the 10 ms burst; slack for a busy host
+
+
+def test_loopback_server_round_trip(tmp_path):
+    """Store -> server -> fetch_chunk over loopback TCP (no GPU): payload and
+    metadata arrive intact, unknown chunks and classes map to the reference errors."""
+    rng = np.random.default_rng(4)
+    meta = {"layout": L.identity_layout(4, 8).to_json(), "F": 4, "plans": {}, "frame_counts": {},
+            "group_size": 8, "scales_b64": ""}
+    payloads = {0: rng.integers(0, 256, 5000).astype(np.uint8).tobytes(),
+                3: rng.integers(0, 256, 70000).astype(np.uint8).tobytes()}
+    cid = bytes(range(16))
+    cont = C.ChunkContainer(cid, 7, 100, 50, 2, meta, payloads)
+    (tmp_path / C.container_filename(cid, 7)).write_bytes(cont.to_bytes())
+    for preload in (False, True):
+        store = NS.ChunkStore(str(tmp_path), preload=preload)
+        assert len(store) == 1
+        with NS.serve(store, ("127.0.0.1", 0), rate_limit_gbps=0.5) as h:
+            addr = f"127.0.0.1:{h.address[1]}"
+            for code, name in ((0, "R240"), (3, "R1080")):
+                payload, got_meta, tau = NS.fetch_chunk(addr, cid, 7, name)
+                assert payload == payloads[code] and tau > 0
+                assert got_meta["resolution"] == name and got_meta["token_start"] == 100
+                assert got_meta["layer_triplet_index"] == 2 and got_meta["cache_id"] == cid.hex()
+                back = NS.container_of(got_meta, payload)
+                assert back.bitstream(code) == payloads[code] and back.token_count == 50
+            with pytest.raises(NS.ChunkNotFound):
+                NS.fetch_chunk(addr, cid, 8, "R240")
+            with pytest.raises(NS.ChunkNotFound):
+                NS.fetch_chunk(addr, cid, 7, "R480")
+            with pytest.raises(NS.ProtocolError):
+                NS.fetch_chunk(addr, cid, 7, 9)
