@@ -133,7 +133,7 @@ typedef struct kvf_pack_unit {
   kvf_paged src;           /* bf16/f16/f32 KV to quantize, or int8 codes */
   kvf_plan plan;
   uint32_t* absmax;        /* device scratch of kvf_pack_scratch_words(&plan) u32:
-                              [3, G] |x| maxima (f32 bit patterns) + [3, G] counters */
+                              [3, G] |x| maxima (f32 bit patterns) + [3, G] step counters */
   float* scales;           /* device [3, G] out (ignored for int8 sources) */
   kvf_surface frames;      /* out: frame_count frames */
 } kvf_pack_unit;
@@ -186,9 +186,23 @@ kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan,
                            const kvf_surface* frames, void* stream);
 
 /* Both phases for up to n_units units, zeroing each unit's scratch first:
- * absmax -> scales -> frames, a handful of launches for any number of units. */
+ * absmax -> scales -> frames (KVF_PACK_AUTO schedule, see kvf_pack_batch_ex). */
 kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
                           void* stream);
+
+/* Pack schedules of kvf_pack_batch_ex. */
+typedef enum kvf_pack_schedule {
+  KVF_PACK_AUTO = 0,        /* the fastest measured on this build (two pass) */
+  KVF_PACK_TWO_PASS = 1,    /* absmax kernel, then frames kernel: reads the source twice */
+  KVF_PACK_SINGLE_READ = 2  /* persistent cooperative grid: slab j's maxima while slab
+                               j-1 (still in L2) is quantised: one HBM read */
+} kvf_pack_schedule;
+
+/* kvf_pack_batch with an explicit schedule.  slab_bytes (single read only) is
+ * the source bytes per pipeline step, 0 = default.  Same results for every
+ * schedule (bit-identical frames and scales). */
+kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
+                             int32_t schedule, int64_t slab_bytes, void* stream);
 
 /* Phase 2 only, for up to n_units units whose `absmax` the caller already
  * filled with the per-(plane, group) maxima of the same source (e.g. a KV

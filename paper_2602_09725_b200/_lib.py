@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libkvf.so")
 
 KVF_OK, KVF_EINVAL, KVF_ECUDA, KVF_EUNSUPPORTED, KVF_EDECODE = range(5)
 KVF_BF16, KVF_F16, KVF_F32, KVF_I8 = range(4)
+KVF_PACK_AUTO, KVF_PACK_TWO_PASS, KVF_PACK_SINGLE_READ = range(3)
 KVF_MAX_UNITS = 128
 ABI_VERSION = 1
 
@@ -146,6 +147,8 @@ _SIGNATURES = {
                                   C.POINTER(kvf_surface), _VP]),
     "kvf_pack_batch": (C.c_int, [C.POINTER(kvf_pack_unit), C.c_int32, _VP]),
     "kvf_pack_frames_batch": (C.c_int, [C.POINTER(kvf_pack_unit), C.c_int32, _VP]),
+    "kvf_pack_batch_ex": (C.c_int, [C.POINTER(kvf_pack_unit), C.c_int32, C.c_int32, C.c_int64,
+                                    _VP]),
     "kvf_pack_scratch_words": (C.c_int64, [C.POINTER(kvf_plan)]),
     "kvf_quantize": (C.c_int, [_VP, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                _VP, _VP, _VP, _VP]),

@@ -199,6 +199,19 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None,
     see the frames after it.  Calls on one stream must come from one thread
     at a time (the device scratch is per stream).
     """
+    staged = []   # the pinned staging buffer, once acquired
+    try:
+        return _decode_batch(streams, out, stream, ranges, indices, max_parts, staged)
+    except BaseException:
+        if staged:
+            # copies queued on side streams may still read the staging buffer:
+            # let every queued copy finish before it can be handed out again
+            torch.cuda.synchronize()
+            _STAGING.release(staged[0])
+        raise
+
+
+def _decode_batch(streams, out, stream, ranges, indices, max_parts, staged):
     dev = _dev.device()
     pinned_in = all(isinstance(x, torch.Tensor) for x in streams) and len(streams) > 0
     datas = list(streams) if pinned_in else [_as_bytes(x) for x in streams]
@@ -242,6 +255,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None,
         parts = _split_parts(live, [sizes[j] for j in live], max_parts)
         if not pinned_in:
             host = _STAGING.acquire(int(starts[-1]) or 1)
+            staged.append(s)
             hv = host.numpy()
             for d, s0, (lo, hi) in zip(datas, starts[:-1], spans):
                 hv[s0:s0 + hi - lo] = np.frombuffer(d, np.uint8, hi - lo, lo)
@@ -298,6 +312,7 @@ def decode_batch(streams, out=None, stream=None, ranges=None, indices=None,
     for t, ev in done:
         s.wait_event(ev)
     if host is not None:
+        staged.clear()
         _STAGING.release(s)   # `s` now follows every part's copies
     held = blob.numel() + symbols.numel() + sum(f.numel() for f in frames)
     # pinned descriptors: alive until `s` passes this point

@@ -228,6 +228,18 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
                : "l"(p));
   return v;
 }
+// Plain load that leaves the line in L2 with the normal eviction priority.
+// (Measured on B200, tools/l2_probe2.cu: a re-read after an
+// ld.global.nc.L1::no_allocate misses L2 as if the line had been evicted at
+// once; after a plain ld.global, or a .nc load with an evict_last policy, a
+// 48 MB re-read runs at ~9 TB/s.)
+__device__ __forceinline__ uint4 ld_keep_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -276,6 +288,11 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst_smem, const void* src, ui
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {

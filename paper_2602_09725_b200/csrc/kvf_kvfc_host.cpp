@@ -52,11 +52,17 @@ extern "C" kvf_status kvf_kvfc_scan(const uint8_t* data, int64_t size, kvf_kvfc_
   info->height = (int32_t)h;
   info->width = (int32_t)w;
   info->bitmap_len = (int32_t)blen;
-  if (cap_frames < (int64_t)n) {  // size query: the walk (and its checks) runs on the fill call
+  // A frame takes at least 13 bytes (type + three u32 lengths): a header that
+  // claims more frames than the bytes can hold is truncated, and the walk below
+  // (without filling) finds the frame decode_frames would raise at.  Callers
+  // size their arrays from n only after this check, so a corrupt header cannot
+  // make them allocate n-sized arrays.
+  const bool fits = 13 * (int64_t)n + 12 <= size;
+  if (cap_frames < (int64_t)n && fits) {  // size query: the walk runs on the fill call
     kvf::set_error("arrays hold %d frames, stream has %u", cap_frames, n);
     return KVF_EINVAL;
   }
-  const bool fill = true;
+  const bool fill = fits;
   int64_t pos = 12;
   for (int32_t f = 0; f < (int32_t)n; ++f) {
     if (pos >= size) return decode_error(bad_frame, f, "stream truncated");

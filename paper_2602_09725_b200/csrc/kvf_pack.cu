@@ -7,36 +7,23 @@
 // kvf_pack_batch runs, per group of units sharing (variant, dtype):
 //   zero scratch -> absmax (max |x| per (plane, group) over all chunk tokens) ->
 //   scales -> frames (exact quantise + tile + place, pad tiles 128).
-// The reference scale spans all chunk tokens, so the source is read twice;
-// KVF_PACK_MODE=team selects the single-HBM-read team kernel
-// (kvf_pack_team.cu), measured slower on B200.
+// The reference scale spans all chunk tokens, so these kernels read the source
+// twice; the single-HBM-read schedule is kvf_pack_persist.cu.
 #include <algorithm>
 #include <cstdio>
-#include <cstdlib>
-#include <cstring>
 #include <vector>
 
 #include "kvf_pack_common.cuh"
 
 namespace kvf {
 
-kvf_status launch_pack_team(const std::vector<kvf_pack_unit>& units, int32_t dtype,
-                            cudaStream_t s, bool* launched);
+kvf_status launch_pack_persist(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+                               int64_t slab_bytes, cudaStream_t s, bool* launched);
 
 namespace {
 
 constexpr int kThreads = kPackThreads;
 constexpr int kWarps = kPackWarps;
-constexpr int kIPW = 8;         // frame items per warp (phase-split frames kernel)
-// absmax tokens per warp (phase-split absmax kernel): 8 for C >= 1024 channels,
-// more for narrow slots so a CTA still reads ~128 KB
-__host__ __device__ constexpr int tok_per_warp(int vpl) { return vpl >= 4 ? 8 : 32 / vpl; }
-
-template <int SRC, int VPL>
-__host__ __device__ constexpr int pack_sub() {
-  return (SRC != KVF_I8 && VPL < 4) ? 4 / VPL : 1;
-}
-
 struct PackParams {
   int32_t n_units;
   PackUnitDev u[kMaxPackUnits];
@@ -52,21 +39,6 @@ __global__ void finalize_scales_kernel(const __grid_constant__ PackParams P) {
   const PackUnitDev& U = P.u[blockIdx.y];
   for (int k = threadIdx.x; k < 3 * U.G; k += blockDim.x)
     U.scales[k] = scale_from_absmax_bits(U.absmax[k]);
-}
-
-// Warp-group reduction of per-lane maxima into s_max[group] (lanes lane+32k of
-// one group are gs/8 consecutive lanes when gs <= 256, else the whole warp).
-template <int SRC, int VPL>
-__device__ __forceinline__ void reduce_groups(const uint32_t (&m)[VPL], int group_size,
-                                              uint32_t* s_max) {
-  const int lane = threadIdx.x & 31;
-  const int lpg = group_size >> 3;
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    uint32_t v = absmax_to_f32_bits<SRC>(m[k]);
-    for (int o = 1; o < 32 && o < lpg; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if ((lane & (min(lpg, 32) - 1)) == 0 && v) atomicMax(&s_max[(lane + 32 * k) / lpg], v);
-  }
 }
 
 // -------------------------------------------------------------------- phase 1
@@ -138,114 +110,14 @@ __global__ void __launch_bounds__(kThreads, 4)
     pack_fast_kernel(const __grid_constant__ PackParams P) {
   const PackUnitDev& U = P.u[blockIdx.y];
   const int p = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Narrow slots (VPL 1 / 2) run SUB items side by side, LPI lanes each, so a
-  // lane still handles 4 vectors per item round (as in restore).
+  const int warp = threadIdx.x >> 5;
   constexpr int SUB = pack_sub<SRC, VPL>();
-  constexpr int LPI = 32 / SUB;
-  constexpr int VL = VPL * SUB;
-  const int sub = lane / LPI, sl = lane % LPI;
   const int item0 = (blockIdx.x * kWarps + warp) * kIPW * SUB;
   if (item0 >= U.n_items) return;
-  constexpr int ES = SRC == KVF_F32 ? 4 : (SRC == KVF_I8 ? 1 : 2);
-  const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
-  int32_t in_off[VL], tile_off[VL];
-  float s[VL], inv[VL];
-#pragma unroll
-  for (int k = 0; k < VL; ++k) {
-    int c = (sl + LPI * k) * 8;
-    in_off[k] = (int32_t)slot_channel_offset(U.g, c, U.src.head_stride) * ES;
-    tile_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
-    if constexpr (SRC != KVF_I8) {
-      s[k] = U.scales[p * U.G + (c >> U.g.lg_gs)];
-      inv[k] = __frcp_rn(s[k]);
-    }
-  }
-  uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
-  // Item q -> (tile origin in the plane, source slot or null for a pad tile).
-  auto locate = [&](int q, uint8_t*& dst, const char*& srcp) {
-    const int f = fdiv(U.g.div_tpf, q);
-    const int slot = q - f * U.g.tpf;
-    const int i = token_of(U.g, f, slot);
-    const int tr = fdiv(U.g.div_cols, slot);
-    const int tc = slot - tr * U.g.grid_cols;
-    dst = plane_base + (int64_t)f * U.fr.frame_stride +
-          (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w;
-    srcp = (i < U.g.T && layer != nullptr)
-               ? layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES
-               : nullptr;
-  };
-  if constexpr (SRC == KVF_I8 || VPL > 4) {
-    for (int it = 0; it < kIPW; ++it) {
-      const int q = item0 + it;
-      if (q >= U.n_items) break;
-      uint8_t* dst;
-      const char* slotp;
-      locate(q, dst, slotp);
-      if (slotp == nullptr) {
-#pragma unroll
-        for (int k = 0; k < VL; ++k)
-          st_v2(dst + tile_off[k], make_uint2(0x80808080u, 0x80808080u));
-        continue;
-      }
-      if constexpr (SRC == KVF_I8) {
-        uint2 v[VL];
-#pragma unroll
-        for (int k = 0; k < VL; ++k) v[k] = ld_nc_v2(slotp + in_off[k]);
-#pragma unroll
-        for (int k = 0; k < VL; ++k)
-          st_v2(dst + tile_off[k], make_uint2(v[k].x ^ 0x80808080u, v[k].y ^ 0x80808080u));
-      } else {
-#pragma unroll
-        for (int k0 = 0; k0 < VL; k0 += 4) {  // at most 32 live values per lane
-          float x[4][8];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) load_vec8<SRC>(slotp + in_off[k0 + k], x[k]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            st_v2(dst + tile_off[k0 + k], quantize8<kRange>(x[k], s[k0 + k], inv[k0 + k]));
-        }
-      }
-    }
-  } else {
-    // Software pipeline: the loads of item it+1 are in flight while item it is
-    // quantised and stored.
-    Raw8<SRC> cur[VL], nxt[VL];
-    uint8_t* dst_cur = nullptr;
-    const char* src_cur = nullptr;
-    const int n_it = min(kIPW, (U.n_items - item0 + SUB - 1) / SUB);  // warp-uniform rounds
-    if (SUB == 1 || item0 + sub < U.n_items) locate(item0 + sub, dst_cur, src_cur);
-    if (src_cur)
-#pragma unroll
-      for (int k = 0; k < VL; ++k) cur[k] = load_raw8<SRC>(src_cur + in_off[k]);
-    for (int it = 0; it < n_it; ++it) {
-      uint8_t* dst_nxt = nullptr;
-      const char* src_nxt = nullptr;
-      const int qn = item0 + (it + 1) * SUB + sub;
-      if (it + 1 < n_it && (SUB == 1 || qn < U.n_items)) {
-        locate(qn, dst_nxt, src_nxt);
-        if (src_nxt)
-#pragma unroll
-          for (int k = 0; k < VL; ++k) nxt[k] = load_raw8<SRC>(src_nxt + in_off[k]);
-      }
-      if (SUB == 1 || dst_cur != nullptr) {  // SUB == 1: every round's item exists
-#pragma unroll
-        for (int k = 0; k < VL; ++k) {
-          uint2 out = make_uint2(0x80808080u, 0x80808080u);
-          if (src_cur) {
-            float x[8];
-            raw8_to_float<SRC>(cur[k], x);
-            out = quantize8<kRange>(x, s[k], inv[k]);
-          }
-          st_v2(dst_cur + tile_off[k], out);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < VL; ++k) cur[k] = nxt[k];
-      dst_cur = dst_nxt;
-      src_cur = src_nxt;
-    }
-  }
+  PackLane<SRC, VPL> L;
+  L.init(U, p, U.scales + p * U.G);
+  const int rounds = min(kIPW, (U.n_items - item0 + SUB - 1) / SUB);
+  pack_items<SRC, VPL, kRange>(U, p, L, item0, SUB, rounds, U.n_items);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -424,55 +296,44 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32
   return KVF_OK;
 }
 
-// Zero the scratch, then the team kernel per launch-sized slice of units with
-// one group size; slices it cannot take run the phase-split kernels.
-kvf_status launch_team_group(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                             cudaStream_t s) {
-  constexpr size_t kChunk = 88;  // units per team launch (kMaxTeamUnits)
+// Single-read schedule: zero the scratch, then one persistent launch per
+// launch-sized slice of units; slices it cannot take run the phase-split kernels.
+kvf_status launch_single_read(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+                              int64_t slab_bytes, cudaStream_t s) {
   std::vector<kvf_pack_unit> rest;
-  std::vector<std::vector<kvf_pack_unit>> by_gs;
-  for (const auto& u : units) {
-    bool placed = false;
-    for (auto& b : by_gs)
-      if (b[0].plan.group_size == u.plan.group_size) {
-        b.push_back(u);
-        placed = true;
-        break;
-      }
-    if (!placed) by_gs.push_back({u});
+  for (size_t at = 0; at < units.size(); at += kMaxPackUnits) {
+    const size_t n = std::min<size_t>(kMaxPackUnits, units.size() - at);
+    std::vector<kvf_pack_unit> part(units.begin() + at, units.begin() + at + n);
+    kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero maxima + counters
+    if (st != KVF_OK) return st;
+    bool launched = false;
+    st = launch_pack_persist(part, vpl, dtype, slab_bytes, s, &launched);
+    if (st != KVF_OK) return st;
+    if (!launched) rest.insert(rest.end(), part.begin(), part.end());
   }
-  for (const auto& b : by_gs)
-    for (size_t at = 0; at < b.size(); at += kChunk) {
-      size_t n = std::min(kChunk, b.size() - at);
-      std::vector<kvf_pack_unit> part(b.begin() + at, b.begin() + at + n);
-      kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero maxima + counters
-      if (st != KVF_OK) return st;
-      bool launched = false;
-      st = launch_pack_team(part, dtype, s, &launched);
-      if (st != KVF_OK) return st;
-      if (!launched) rest.insert(rest.end(), part.begin(), part.end());
-    }
   return rest.empty() ? KVF_OK : launch_phases(rest, vpl, dtype, 2 | 4 | 8, s);
 }
 
-kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, cudaStream_t s) {
+kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t schedule,
+               int64_t slab_bytes, cudaStream_t s) {
   if (n_units < 0 || (n_units > 0 && units == nullptr)) KVF_FAIL(KVF_EINVAL, "bad unit array");
+  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_SINGLE_READ)
+    KVF_FAIL(KVF_EINVAL, "bad pack schedule %d", schedule);
+  if (slab_bytes < 0) KVF_FAIL(KVF_EINVAL, "negative slab_bytes");
   std::vector<kvf_pack_unit> groups[17][4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
     if (st != KVF_OK) return st;
     groups[pack_variant(units[k])][units[k].src.dtype].push_back(units[k]);
   }
+  // AUTO = the two-pass kernels: fastest measured on B200 so far
+  const bool single = schedule == KVF_PACK_SINGLE_READ && phases == (1 | 2 | 4 | 8);
   for (int v = 0; v <= 16; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        // Default: the phase-split kernels (fastest measured);
-        // KVF_PACK_MODE=team selects the single-HBM-read team kernel.
-        const char* mode = getenv("KVF_PACK_MODE");
-        const bool team = v != 0 && dt != KVF_I8 && phases == (1 | 2 | 4 | 8) && mode &&
-                          strcmp(mode, "team") == 0;
-        kvf_status st = team ? launch_team_group(groups[v][dt], v, dt, s)
-                             : launch_phases(groups[v][dt], v, dt, phases, s);
+        kvf_status st = (single && v != 0 && dt != KVF_I8)
+                            ? launch_single_read(groups[v][dt], v, dt, slab_bytes, s)
+                            : launch_phases(groups[v][dt], v, dt, phases, s);
         if (st != KVF_OK) return st;
       }
   return KVF_OK;
@@ -503,12 +364,19 @@ kvf_pack_unit single(const kvf_paged* src, const kvf_plan* plan, const uint32_t*
 using namespace kvf;
 
 extern "C" kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units, void* stream) {
-  return run(units, n_units, 1 | 2 | 4 | 8, reinterpret_cast<cudaStream_t>(stream));
+  return run(units, n_units, 1 | 2 | 4 | 8, KVF_PACK_AUTO, 0,
+             reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
+                                        int32_t schedule, int64_t slab_bytes, void* stream) {
+  return run(units, n_units, 1 | 2 | 4 | 8, schedule, slab_bytes,
+             reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" kvf_status kvf_pack_frames_batch(const kvf_pack_unit* units, int32_t n_units,
                                             void* stream) {
-  return run(units, n_units, 4 | 8, reinterpret_cast<cudaStream_t>(stream));
+  return run(units, n_units, 4 | 8, KVF_PACK_AUTO, 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" kvf_status kvf_pack_absmax(const kvf_paged* src, const kvf_plan* plan,
@@ -517,7 +385,7 @@ extern "C" kvf_status kvf_pack_absmax(const kvf_paged* src, const kvf_plan* plan
   if (src->dtype == KVF_I8) KVF_FAIL(KVF_EINVAL, "int8 codes have no absmax phase");
   float unused_scales;
   kvf_pack_unit u = single(src, plan, absmax, &unused_scales, nullptr);
-  return run(&u, 1, 2, reinterpret_cast<cudaStream_t>(stream));
+  return run(&u, 1, 2, KVF_PACK_AUTO, 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan,
@@ -525,7 +393,7 @@ extern "C" kvf_status kvf_pack_frames(const kvf_paged* src, const kvf_plan* plan
                                       const kvf_surface* frames, void* stream) {
   if (!src || !plan || !frames) KVF_FAIL(KVF_EINVAL, "null argument");
   kvf_pack_unit u = single(src, plan, absmax, scales, frames);
-  return run(&u, 1, 4 | 8, reinterpret_cast<cudaStream_t>(stream));
+  return run(&u, 1, 4 | 8, KVF_PACK_AUTO, 0, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int64_t kvf_pack_scratch_words(const kvf_plan* plan) {

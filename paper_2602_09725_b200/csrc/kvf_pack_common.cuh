@@ -1,5 +1,6 @@
-// kvf_pack_common.cuh — pieces shared by the phase-split and team pack kernels:
-// unit descriptor, source vector loads, |x| maxima, and the exact quantiser.
+// kvf_pack_common.cuh — pieces shared by the phase-split and the single-read
+// (persistent) pack kernels: unit descriptor, source vector loads, |x| maxima,
+// the exact quantiser and the per-warp frame-item loop.
 //
 // Quantisation is the reference's (fk/kvmodel.py:127-144): per (layer, group)
 // scale = fp32(fp64(max|x|)/127) or 1.0, q = clip(rint_half_even(fp64 x / fp64 s),
@@ -15,7 +16,8 @@ constexpr int kPackWarps = kPackThreads / 32;
 constexpr int kMaxPackUnits = 96;  // descriptors per launch (kernel params <= 32 KB)
 
 // Scratch words of a unit (kvf_pack_scratch_words): [3, G] |x| maxima (f32
-// bit patterns) | [3, G] per-(plane, group) counters of the team kernel.
+// bit patterns) | [3, G] words of step counters (the single-read kernel keeps
+// one counter per slab in the first word of its first (unit, plane)).
 inline int64_t pack_scratch_words(const kvf_plan& p) {
   const int64_t G = (int64_t)p.H * p.D / p.group_size;
   return 6 * G;
@@ -25,7 +27,7 @@ struct PackUnitDev {
   kvf_paged src;
   Geom g;
   uint32_t* absmax;       // [3, G] maxima (f32 bit patterns)
-  uint32_t* team_done;    // absmax + 3G: [3, G] per-(plane, group) team counters
+  uint32_t* counters;     // absmax + 3G: [3, G] counter words
   float* scales;
   kvf_surface fr;
   FastDiv div_bs;
@@ -40,7 +42,7 @@ inline PackUnitDev make_pack_unit_dev(const kvf_pack_unit& u) {
   d.g = make_geom(u.plan);
   d.G = (u.plan.H * u.plan.D) / u.plan.group_size;
   d.absmax = u.absmax;
-  d.team_done = u.absmax ? u.absmax + 3 * d.G : nullptr;
+  d.counters = u.absmax ? u.absmax + 3 * d.G : nullptr;
   d.n_scratch = (int32_t)pack_scratch_words(u.plan);
   d.scales = u.scales;
   d.fr = u.frames;
@@ -49,18 +51,16 @@ inline PackUnitDev make_pack_unit_dev(const kvf_pack_unit& u) {
   return d;
 }
 
-// Source vector loads; the team kernel tags its re-reads with an L2 eviction policy.
+// Source vector loads (optionally tagged with an L2 eviction policy).
 struct NoPolicy {
   __device__ __forceinline__ uint4 load(const char* p) const { return ld_nc_v4(p); }
+};
+struct KeepLoad {  // coherent path: the line stays in L2 for a re-read
+  __device__ __forceinline__ uint4 load(const char* p) const { return ld_keep_v4(p); }
 };
 struct WithPolicy {
   uint64_t pol;
   __device__ __forceinline__ uint4 load(const char* p) const { return ld_nc_v4_pol(p, pol); }
-};
-struct SmemLoad {  // data staged in shared memory
-  __device__ __forceinline__ uint4 load(const char* p) const {
-    return *reinterpret_cast<const uint4*>(p);
-  }
 };
 
 // max |x| bit pattern over 8 values (16-bit patterns for bf16/fp16, which order
@@ -216,6 +216,165 @@ __device__ __forceinline__ uint2 quantize8(const float (&x)[8], float s, float i
   if (__builtin_expect(bad, 0))
     out = quantize8_exact(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], s, inv);
   return out;
+}
+
+// ------------------------------------------------------------ frame items
+constexpr int kIPW = 8;  // frame items per warp run
+
+// absmax tokens per warp (phase-split absmax kernel): 8 for C >= 1024 channels,
+// more for narrow slots so a CTA still reads ~128 KB
+__host__ __device__ constexpr int tok_per_warp(int vpl) { return vpl >= 4 ? 8 : 32 / vpl; }
+
+// Narrow slots (VPL 1 / 2) run SUB items side by side in a warp, 32/SUB lanes
+// each, so a lane still handles 4 vectors per item round (as in restore).
+template <int SRC, int VPL>
+__host__ __device__ constexpr int pack_sub() {
+  return (SRC != KVF_I8 && VPL < 4) ? 4 / VPL : 1;
+}
+
+// Warp-group reduction of per-lane maxima into s_max[group] (lanes lane+32k of
+// one group are gs/8 consecutive lanes when gs <= 256, else the whole warp).
+template <int SRC, int VPL>
+__device__ __forceinline__ void reduce_groups(const uint32_t (&m)[VPL], int group_size,
+                                              uint32_t* s_max) {
+  const int lane = threadIdx.x & 31;
+  const int lpg = group_size >> 3;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    uint32_t v = absmax_to_f32_bits<SRC>(m[k]);
+    for (int o = 1; o < 32 && o < lpg; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((lane & (min(lpg, 32) - 1)) == 0 && v) atomicMax(&s_max[(lane + 32 * k) / lpg], v);
+  }
+}
+
+// Per-lane constants of one (unit, plane) for the frame-item loop: source and
+// tile offsets of the lane's 8-channel vectors and their group scales.
+template <int SRC, int VPL>
+struct PackLane {
+  static constexpr int SUB = pack_sub<SRC, VPL>();
+  static constexpr int LPI = 32 / SUB;
+  static constexpr int VL = VPL * SUB;
+  int32_t in_off[VL], tile_off[VL];
+  float s[VL], inv[VL];
+
+  // `scales`: the plane's [G] scales (ignored for int8 sources).
+  __device__ __forceinline__ void init(const PackUnitDev& U, int p, const float* scales) {
+    constexpr int ES = SRC == KVF_F32 ? 4 : (SRC == KVF_I8 ? 1 : 2);
+    const int sl = (threadIdx.x & 31) % LPI;
+#pragma unroll
+    for (int k = 0; k < VL; ++k) {
+      const int c = (sl + LPI * k) * 8;
+      in_off[k] = (int32_t)slot_channel_offset(U.g, c, U.src.head_stride) * ES;
+      tile_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
+      if constexpr (SRC != KVF_I8) {
+        s[k] = scales[c >> U.g.lg_gs];
+        inv[k] = __frcp_rn(s[k]);
+      }
+    }
+  }
+};
+
+// One warp packs frame items of plane p in `rounds` rounds: round r takes items
+// item0 + r*stride + sub (sub < SUB, lanes split SUB ways), those below `end`.
+// Item q = (frame, tile slot) -> its token's quantised slot at the tile origin,
+// or a pad tile of 128s.  Rounds are software-pipelined (the loads of round
+// r+1 are in flight while round r is quantised and stored).
+template <int SRC, int VPL, bool kRange, typename LD = NoPolicy>
+__device__ __forceinline__ void pack_items(const PackUnitDev& U, int p,
+                                           const PackLane<SRC, VPL>& L, int item0, int stride,
+                                           int rounds, int end, LD ld = LD()) {
+  constexpr int SUB = PackLane<SRC, VPL>::SUB;
+  constexpr int LPI = PackLane<SRC, VPL>::LPI;
+  constexpr int VL = PackLane<SRC, VPL>::VL;
+  constexpr int ES = SRC == KVF_F32 ? 4 : (SRC == KVF_I8 ? 1 : 2);
+  const int sub = (threadIdx.x & 31) / LPI;
+  const char* layer = reinterpret_cast<const char*>(U.src.layer[p]);
+  uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
+  // Item q -> (tile origin in the plane, source slot or null for a pad tile).
+  auto locate = [&](int q, uint8_t*& dst, const char*& srcp) {
+    const int f = fdiv(U.g.div_tpf, q);
+    const int slot = q - f * U.g.tpf;
+    const int i = token_of(U.g, f, slot);
+    const int tr = fdiv(U.g.div_cols, slot);
+    const int tc = slot - tr * U.g.grid_cols;
+    dst = plane_base + (int64_t)f * U.fr.frame_stride +
+          (int64_t)tr * U.g.tile_h * U.fr.row_pitch + (int64_t)tc * U.g.tile_w;
+    srcp = (i < U.g.T && layer != nullptr)
+               ? layer + paged_slot_offset_fd(U.src, U.div_bs, i) * ES
+               : nullptr;
+  };
+  if constexpr (SRC == KVF_I8 || VPL > 4) {
+    for (int it = 0; it < rounds; ++it) {
+      const int q = item0 + it * stride + sub;
+      if (q >= end) break;
+      uint8_t* dst;
+      const char* slotp;
+      locate(q, dst, slotp);
+      if (slotp == nullptr) {
+#pragma unroll
+        for (int k = 0; k < VL; ++k)
+          st_v2(dst + L.tile_off[k], make_uint2(0x80808080u, 0x80808080u));
+        continue;
+      }
+      if constexpr (SRC == KVF_I8) {
+        uint2 v[VL];
+#pragma unroll
+        for (int k = 0; k < VL; ++k) v[k] = ld_nc_v2(slotp + L.in_off[k]);
+#pragma unroll
+        for (int k = 0; k < VL; ++k)
+          st_v2(dst + L.tile_off[k], make_uint2(v[k].x ^ 0x80808080u, v[k].y ^ 0x80808080u));
+      } else {
+#pragma unroll
+        for (int k0 = 0; k0 < VL; k0 += 4) {  // at most 32 live values per lane
+          float x[4][8];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) load_vec8<SRC>(slotp + L.in_off[k0 + k], x[k], ld);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            st_v2(dst + L.tile_off[k0 + k],
+                  quantize8<kRange>(x[k], L.s[k0 + k], L.inv[k0 + k]));
+        }
+      }
+    }
+  } else {
+    // Software pipeline: the loads of item it+1 are in flight while item it is
+    // quantised and stored.
+    Raw8<SRC> cur[VL], nxt[VL];
+    uint8_t* dst_cur = nullptr;
+    const char* src_cur = nullptr;
+    const int n_it = rounds;  // warp-uniform
+    if (item0 + sub < end) locate(item0 + sub, dst_cur, src_cur);
+    if (src_cur)
+#pragma unroll
+      for (int k = 0; k < VL; ++k) cur[k] = load_raw8<SRC>(src_cur + L.in_off[k], ld);
+    for (int it = 0; it < n_it; ++it) {
+      uint8_t* dst_nxt = nullptr;
+      const char* src_nxt = nullptr;
+      const int qn = item0 + (it + 1) * stride + sub;
+      if (it + 1 < n_it && qn < end) {
+        locate(qn, dst_nxt, src_nxt);
+        if (src_nxt)
+#pragma unroll
+          for (int k = 0; k < VL; ++k) nxt[k] = load_raw8<SRC>(src_nxt + L.in_off[k], ld);
+      }
+      if (dst_cur != nullptr) {
+#pragma unroll
+        for (int k = 0; k < VL; ++k) {
+          uint2 out = make_uint2(0x80808080u, 0x80808080u);
+          if (src_cur) {
+            float x[8];
+            raw8_to_float<SRC>(cur[k], x);
+            out = quantize8<kRange>(x, L.s[k], L.inv[k]);
+          }
+          st_v2(dst_cur + L.tile_off[k], out);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < VL; ++k) cur[k] = nxt[k];
+      dst_cur = dst_nxt;
+      src_cur = src_nxt;
+    }
+  }
 }
 
 }  // namespace kvf

@@ -320,6 +320,10 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
     state = {"dec_end": None}
     pool = _RECEIVE_POOL
     claim_lock = threading.Lock()   # PagedMemory host state + timeline bookkeeping
+    # The CUDA current device is per thread and a new thread starts on device 0:
+    # the worker threads adopt the caller's device (a rank that called
+    # torch.cuda.set_device(k) keeps all its streams, scratch and restores on k).
+    dev_index = torch.cuda.current_device()
 
     def launch_batch(items, gpu_stream, frame_buf, peers=()):
         """Queue one batch's decode + restore on the worker stream; returns the
@@ -404,6 +408,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
         """Takes every chunk received so far as one batch and queues it on its
         own stream while earlier batches still run (at most _INFLIGHT), so
         host preparation and the batches' GPU work overlap."""
+        torch.cuda.set_device(dev_index)
         streams, frame_bufs, slot_lock = _worker_context(slot)
         with slot_lock:  # concurrent fetches on this slot take turns
             with torch.cuda.stream(streams[0]):

@@ -205,6 +205,11 @@ class PagedMemory:
             grown = torch.empty((new_cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
             grown[: t.shape[0]].copy_(t)
             self.layers[k] = grown
+        if self._cap_blocks and self.layers:
+            # the copies ran on the current stream; restores queued later on other
+            # streams (a fetcher rotates several) must not overtake them, and the
+            # old pools must not be recycled while a copy still reads them
+            torch.cuda.synchronize()
         self._free.extend(range(new_cap - 1, self._cap_blocks - 1, -1))
         self._cap_blocks = new_cap
 
