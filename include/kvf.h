@@ -278,7 +278,10 @@ typedef struct kvf_recon_plane {
 } kvf_recon_plane;
 
 /* A dependency chain: planes[first .. first+count) of ONE plane index over
- * consecutive frames, the first intra; entry k predicts from entry k-1. */
+ * consecutive frames, the first intra; entry k predicts from entry k-1.  An
+ * entry with symbols == NULL is a plane reconstructed by an earlier call (the
+ * previous frame of a frame-by-frame decode): it is not written, only read as
+ * the next entry's reference, so a chain may start [reference, inter plane]. */
 typedef struct kvf_recon_chain {
   int32_t first;
   int32_t count;

@@ -35,7 +35,8 @@ def to_device(x, dtype: torch.dtype | None = None) -> torch.Tensor:
     current stream (stream-ordered for every later use; a pageable copy would
     block the host until all work already queued on the stream finished)."""
     if isinstance(x, np.ndarray):
-        x = torch.from_numpy(np.ascontiguousarray(x))
+        x = np.ascontiguousarray(x)
+        x = torch.from_numpy(x if x.flags.writeable else x.copy())
     if not isinstance(x, torch.Tensor):
         x = torch.as_tensor(x)
     if dtype is not None and x.dtype != dtype:

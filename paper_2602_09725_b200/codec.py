@@ -518,19 +518,91 @@ def _side_streams(stream, n):
         return pool[:n]
 
 
-def decode_frames(bs, cfg: CodecConfig, on_frame, stats=None):
-    """Decode a Bitstream (or raw bytes) on the GPU, calling on_frame(index, frame).
+def decode_stream_framewise(bs, on_frame, stream=None, index=None) -> int:
+    """Decode one KVFC stream frame by frame on the GPU (fk/codec.py:155-211).
 
-    ``frame`` is a [3, h, w] uint8 CUDA tensor view.  stats["peak_live_bytes"]
-    reports the device bytes held by the decode (stream, symbols, frames).
+    Per frame: one range-decode launch for its three plane streams and one
+    reconstruction launch whose chains are [previous frame's plane (reference
+    only), this frame's plane], so only the current and the previous frame are
+    held, as in the reference decoder.  ``on_frame(f, frame)`` gets a [3, h, w]
+    uint8 CUDA view of a buffer that frame f + 2 reuses: work it queues on the
+    decode stream (``stream``, default current) is ordered before that reuse; a
+    callback that keeps the frame must clone it.  All descriptors are built up
+    front (vectorised) and read in place from pinned host memory.  Returns the
+    frame count; raises DecodeError like the reference.
     """
-    frames, held = decode_batch([bs])
-    fr = frames[0]
-    for f in range(fr.shape[0]):
-        on_frame(f, fr[f])
+    data = bs if isinstance(bs, torch.Tensor) else _as_bytes(bs)
+    ix = index if index is not None else StreamIndex(data)
+    n, h, w = ix.n, ix.h, ix.w
+    if n == 0:
+        return 0
+    s = stream if stream is not None else torch.cuda.current_stream()
+    dev = _dev.device()
+    hw = h * w
+    hw16 = -(-hw // 16) * 16
+    with torch.cuda.stream(s):
+        # the coded bytes travel once; frames are decoded into two buffers
+        host = torch.frombuffer(bytearray(data), dtype=torch.uint8) if not isinstance(
+            data, torch.Tensor) else data
+        blob = torch.empty(max(host.numel(), 1), dtype=torch.uint8, device=dev)
+        blob[:host.numel()].copy_(host.pin_memory() if not host.is_pinned() else host,
+                                  non_blocking=True)
+        symbols = torch.empty(max(3 * hw16, 16), dtype=torch.uint8, device=dev)
+        bufs = torch.empty((2, 3, h, w), dtype=torch.uint8, device=dev)
+    k = np.arange(3 * n, dtype=np.int64)
+    f, p = k // 3, k % 3
+    base = blob.data_ptr()
+    rc = np.empty(3 * n, _RC_DTYPE)
+    rc["payload"] = base + ix.payload_off
+    rc["len"] = ix.payload_len
+    rc["symbols"] = symbols.data_ptr() + p * hw16
+    rc["n_symbols"] = hw
+    # planes [n, 3, 2]: (reference entry, this frame's entry) per plane
+    fb = bufs.data_ptr() + p * hw
+    pl = np.zeros((3 * n, 2), _PLANE_DTYPE)
+    pl["out_pitch"] = w
+    pl["out"][:, 0] = fb + ((f + 1) % 2) * 3 * hw            # previous frame's buffer
+    pl["symbols"][:, 1] = rc["symbols"]
+    pl["modes"][:, 1] = np.where(ix.bitmap_off >= 0, base + ix.bitmap_off, 0)
+    pl["out"][:, 1] = fb + (f % 2) * 3 * hw
+    inter = ix.frame_type[f] != 0
+    ch = np.empty(3 * n, _CHAIN_DTYPE)
+    ch["first"] = 2 * k + np.where(inter, 0, 1)
+    ch["count"] = np.where(inter, 2, 1)
+    ch["height"], ch["width"] = h, w
+    h_rc, h_pl, h_ch = (_pinned_copy(x.reshape(-1)) for x in (rc, pl, ch))
+    rc_sz, ch_sz = _RC_DTYPE.itemsize, _CHAIN_DTYPE.itemsize
+    sp = _dev.stream_ptr(s)
+    try:
+        for fi in range(n):
+            if hw:
+                _lib.call("kvf_rc_decode", C.c_void_p(h_rc.data_ptr() + 3 * fi * rc_sz), 3, sp)
+                _lib.call("kvf_kvfc_reconstruct", C.c_void_p(h_pl.data_ptr()),
+                          C.c_void_p(h_ch.data_ptr() + 3 * fi * ch_sz), 3, sp)
+            with torch.cuda.stream(s):
+                on_frame(fi, bufs[fi % 2])
+    finally:
+        _hold_until(s, [h_rc, h_pl, h_ch])
+        for t in (blob, symbols, bufs):
+            t.record_stream(s)
+    return n
+
+
+def decode_frames(bs, cfg: CodecConfig, on_frame, stats=None):
+    """Decode a Bitstream (or raw bytes) on the GPU frame by frame, calling
+    on_frame(index, frame) (fk/codec.py:155-211).
+
+    ``frame`` is a [3, h, w] uint8 CUDA view of a buffer reused two frames
+    later (see decode_stream_framewise).  stats["peak_live_bytes"] is the
+    reference's quantity: decoded-frame bytes retained, i.e. the current frame
+    plus its reference (fk/codec.py:203-210).  For many streams at once use
+    decode_batch.
+    """
+    n = decode_stream_framewise(bs, on_frame)
     if stats is not None:
-        stats["peak_live_bytes"] = held
-    return fr.shape[0]
+        ix_h, ix_w = header(bs)[1:]
+        stats["peak_live_bytes"] = min(n, 2) * 3 * ix_h * ix_w
+    return n
 
 
 def _to_dev_struct(arr: np.ndarray, dev) -> torch.Tensor:

@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kReconThreads)
   const int nwarps = blockDim.x >> 5;
   for (int e = 0; e < ch.count; ++e) {
     const kvf_recon_plane P = planes[ch.first + e];
+    if (P.symbols == nullptr) continue;  // reconstructed earlier: only a reference
     const uint8_t* prev = e > 0 ? planes[ch.first + e - 1].out : nullptr;
     const int64_t prev_pitch = e > 0 ? planes[ch.first + e - 1].out_pitch : 0;
     const uint8_t* modes = e > 0 ? P.modes : nullptr;

@@ -250,8 +250,8 @@ _WORKER_LOCK = threading.Lock()
 
 # batches a GPU worker keeps in flight (one stream + frame buffer each), and the
 # fewest chunks a batch takes while others are in flight
-_INFLIGHT = int(os.environ.get("KVF_FETCH_INFLIGHT", "4"))
-_MIN_BATCH = int(os.environ.get("KVF_FETCH_MIN_BATCH", "4"))
+_INFLIGHT = 4
+_MIN_BATCH = 4
 _LONG_STREAM = 1 << 16   # symbols per stream from which a batch decode is latency-bound
 
 
@@ -281,7 +281,7 @@ def _mem_for(mem, cache_id):
 def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=None,
                         initial_active="R1080", timeout_s=30.0, on_chunk=None, *, mem=None,
                         real_layers=None, depth=32, max_batch=32,
-                        fetch_fn=None, workers=1):
+                        fetch_fn=None, workers=1, max_inflight=None):
     """Fetch chunks from a live server and decode them on the GPU as they arrive.
 
     ``chunks``: list of (cache_id, chunk_index).  Without ``mem`` each chunk is
@@ -307,7 +307,10 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
 
     ``fetch_fn`` replaces the network round trip (default netstore.fetch_chunk,
     same signature); it is how a modelled link is replayed against the real
-    GPU pipeline.
+    GPU pipeline.  ``max_inflight`` caps the batches a worker keeps on the GPU at
+    once (default: 4 for long-stream classes, 2 for R240); ``max_batch=1,
+    max_inflight=1`` is the reference's schedule (one decode at a time on one
+    worker, overlapping the next transfer).
     """
     fetch_fn = fetch_fn or NS.fetch_chunk
     fixed = _fixed_policy(policy)
@@ -446,7 +449,7 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                     # With batches already in flight, a new one waits for at least
                     # _MIN_BATCH chunks (or for the oldest batch to finish): small
                     # batches cost a decode latency each and thin out throughput.
-                    while (inflight and not stop and len(items) < _MIN_BATCH and
+                    while (inflight and not stop and len(items) < min(_MIN_BATCH, max_batch) and
                            not inflight[0]["done"].query()):
                         try:
                             nxt = work.get(timeout=0.0005)
@@ -463,6 +466,8 @@ def live_fetch_pipeline(address, chunks, table, policy="adaptive", prior_gbps=No
                     # _INFLIGHT batches overlap.  Short ones (R240) are
                     # throughput-bound and two in flight keep the GPU busy.
                     limit = _INFLIGHT if long_streams else min(2, _INFLIGHT)
+                    if max_inflight is not None:
+                        limit = max(1, min(int(max_inflight), _INFLIGHT))
                     while len(inflight) >= limit:  # the oldest's stream + buffer are reused
                         finish_batch(inflight.popleft(), clock)
                     j = k % _INFLIGHT

@@ -119,11 +119,16 @@ def restore_stream(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_base
                    token_base=0, *, scales=None, batch_frames=None, real_layers=None):
     """Frame-wise restore of one KVFC stream into paged memory (fk/fetchsim.py:335-358).
 
-    Decodes on the GPU and restores each decoded frame batch with one libkvf
-    launch.  ``batch_frames=None`` decodes the whole chunk at once (maximum
-    decoder parallelism); a small value (e.g. plan.F) bounds the live decode
-    buffers to that many frames, the reference's frame-wise memory profile.
-    Returns {"tokens_written", "peak_buffer_bytes"} like the reference.
+    Default (``batch_frames=None``): the reference's On_frame_probe.  The GPU
+    decodes the stream frame by frame (codec.decode_stream_framewise: only the
+    current frame and its reference are held) and each decoded frame's tile
+    slots are restored with one libkvf launch as soon as it is reconstructed
+    (un-tile, -128, dequantise with ``scales`` unless the cache holds int8
+    codes, paged scatter).  ``batch_frames=k`` decodes runs of >= k frames
+    that start at intra frames in one decode_batch each (more decoder
+    parallelism, more live frames).  Returns {"tokens_written",
+    "peak_buffer_bytes"} with the reference's peak: decoded-frame bytes
+    retained at once (fk/codec.py:203-210).
     """
     from . import codec
 
@@ -131,11 +136,23 @@ def restore_stream(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_base
     ix = codec.StreamIndex(data)
     if (ix.n, ix.h, ix.w) != (plan.frame_count, plan.frame_h, plan.frame_w):
         raise ValueError("stream geometry does not match the plan")
-    ranges = [(0, ix.n)] if batch_frames is None else _chain_batches(ix, int(batch_frames))
+    frame_bytes = 3 * ix.h * ix.w
+    if batch_frames is None:
+        if scales is not None and mem.dtype != torch.int8:
+            scales = _dev.to_device(scales, torch.float32).contiguous()
+        written = [0]
+
+        def on_frame(f, frame):
+            written[0] += restore_frames(frame[None], plan, mem, layer_base, token_base,
+                                         scales=scales, first_frame=f, n_frames=1,
+                                         real_layers=real_layers)
+
+        n = codec.decode_stream_framewise(data, on_frame, index=ix)
+        return {"tokens_written": written[0], "peak_buffer_bytes": min(n, 2) * frame_bytes}
     written, peak = 0, 0
-    for f0, f1 in ranges:
-        frames, held = codec.decode_batch([data], ranges=[(f0, f1)], indices=[ix])
-        peak = max(peak, held)
+    for f0, f1 in _chain_batches(ix, int(batch_frames)):
+        frames, _ = codec.decode_batch([data], ranges=[(f0, f1)], indices=[ix])
+        peak = max(peak, (f1 - f0) * frame_bytes)
         written += restore_frames(frames[0], plan, mem, layer_base, token_base, scales=scales,
                                   first_frame=f0, n_frames=f1 - f0, real_layers=real_layers)
     return {"tokens_written": written, "peak_buffer_bytes": peak}
@@ -143,13 +160,17 @@ def restore_stream(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_base
 
 def restore_chunk_wise(bs, plan: FramePlan, cfg_layout, mem: PagedMemory, layer_base=0,
                        token_base=0, *, scales=None, real_layers=None):
-    """Baseline: decode every frame, then restore (fk/fetchsim.py:361-385)."""
+    """Baseline: decode every frame, then restore (fk/fetchsim.py:361-385).
+    peak_buffer_bytes is the reference's: every decoded frame plus the
+    decoder's reference frame."""
     from . import codec
 
-    frames, held = codec.decode_batch([bs])
+    frames, _ = codec.decode_batch([bs])
     written = restore_frames(frames[0], plan, mem, layer_base, token_base, scales=scales,
                              real_layers=real_layers)
-    return {"tokens_written": written, "peak_buffer_bytes": held}
+    n = frames[0].shape[0]
+    return {"tokens_written": written,
+            "peak_buffer_bytes": (n + 1) * frames[0][0].numel() if n else 0}
 
 
 def restore_units(units, stream=None) -> None:
