@@ -133,7 +133,7 @@ typedef struct kvf_pack_unit {
   kvf_paged src;           /* bf16/f16/f32 KV to quantize, or int8 codes */
   kvf_plan plan;
   uint32_t* absmax;        /* device scratch of kvf_pack_scratch_words(&plan) u32:
-                              [3, G] |x| maxima (f32 bit patterns) + [3, G] step counters */
+                              [3, G] |x| maxima (f32 bit patterns) + [3, G] reserved */
   float* scales;           /* device [3, G] out (ignored for int8 sources) */
   kvf_surface frames;      /* out: frame_count frames */
 } kvf_pack_unit;
@@ -192,17 +192,22 @@ kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
 
 /* Pack schedules of kvf_pack_batch_ex. */
 typedef enum kvf_pack_schedule {
-  KVF_PACK_AUTO = 0,        /* the fastest measured on this build (two pass) */
+  KVF_PACK_AUTO = 0,        /* the fastest measured on this build */
   KVF_PACK_TWO_PASS = 1,    /* absmax kernel, then frames kernel: reads the source twice */
-  KVF_PACK_SINGLE_READ = 2  /* persistent cooperative grid: slab j's maxima while slab
-                               j-1 (still in L2) is quantised: one HBM read */
+  KVF_PACK_SINGLE_READ = 2  /* thread-block clusters, one per (unit, plane, group) at a
+                               time, exchange the all-token maxima through distributed
+                               shared memory; the quantising re-read is an L2 hit */
 } kvf_pack_schedule;
 
-/* kvf_pack_batch with an explicit schedule.  slab_bytes (single read only) is
- * the source bytes per pipeline step, 0 = default.  Same results for every
- * schedule (bit-identical frames and scales). */
+/* kvf_pack_batch with an explicit schedule.  `param` (single read only): bits
+ * 0-7 = CTAs per cluster (16, 8, 4 or 2; 0 = the configuration covering the
+ * most SMs while the sub-units in flight fit in ~45% of L2); bit 8 = drop that
+ * L2 cap; bits 9-10 = CTA shape (0: 16 warps x 3 stages, 1: 12 x 4, 2: 8 x 6).
+ * Same results for every schedule (bit-identical frames and scales); units a
+ * schedule cannot take (int8 sources, unsupported group sizes or alignment)
+ * run the two-pass kernels. */
 kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
-                             int32_t schedule, int64_t slab_bytes, void* stream);
+                             int32_t schedule, int64_t param, void* stream);
 
 /* Phase 2 only, for up to n_units units whose `absmax` the caller already
  * filled with the per-(plane, group) maxima of the same source (e.g. a KV

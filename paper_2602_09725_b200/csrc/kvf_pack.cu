@@ -8,7 +8,7 @@
 //   zero scratch -> absmax (max |x| per (plane, group) over all chunk tokens) ->
 //   scales -> frames (exact quantise + tile + place, pad tiles 128).
 // The reference scale spans all chunk tokens, so these kernels read the source
-// twice; the single-HBM-read schedule is kvf_pack_persist.cu.
+// twice; the single-HBM-read schedule is kvf_pack_cluster.cu.
 #include <algorithm>
 #include <cstdio>
 #include <vector>
@@ -17,8 +17,8 @@
 
 namespace kvf {
 
-kvf_status launch_pack_persist(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                               int64_t slab_bytes, cudaStream_t s, bool* launched);
+kvf_status launch_pack_cluster(const std::vector<kvf_pack_unit>& units, int32_t dtype,
+                               int64_t param, cudaStream_t s, bool* launched);
 
 namespace {
 
@@ -296,44 +296,50 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32
   return KVF_OK;
 }
 
-// Single-read schedule: zero the scratch, then one persistent launch per
-// launch-sized slice of units; slices it cannot take run the phase-split kernels.
-kvf_status launch_single_read(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                              int64_t slab_bytes, cudaStream_t s) {
-  std::vector<kvf_pack_unit> rest;
+// Single-read schedule: one cluster launch per launch-sized slice of units;
+// slices it cannot take run the phase-split kernels.
+kvf_status launch_single_read(const std::vector<kvf_pack_unit>& units, int32_t dtype,
+                              int64_t param, cudaStream_t s,
+                              std::vector<kvf_pack_unit>* rest) {
   for (size_t at = 0; at < units.size(); at += kMaxPackUnits) {
     const size_t n = std::min<size_t>(kMaxPackUnits, units.size() - at);
     std::vector<kvf_pack_unit> part(units.begin() + at, units.begin() + at + n);
-    kvf_status st = launch_phases(part, vpl, dtype, 1, s);  // zero maxima + counters
-    if (st != KVF_OK) return st;
     bool launched = false;
-    st = launch_pack_persist(part, vpl, dtype, slab_bytes, s, &launched);
+    kvf_status st = launch_pack_cluster(part, dtype, param, s, &launched);
     if (st != KVF_OK) return st;
-    if (!launched) rest.insert(rest.end(), part.begin(), part.end());
+    if (!launched) rest->insert(rest->end(), part.begin(), part.end());
   }
-  return rest.empty() ? KVF_OK : launch_phases(rest, vpl, dtype, 2 | 4 | 8, s);
+  return KVF_OK;
 }
 
 kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t schedule,
-               int64_t slab_bytes, cudaStream_t s) {
+               int64_t param, cudaStream_t s) {
   if (n_units < 0 || (n_units > 0 && units == nullptr)) KVF_FAIL(KVF_EINVAL, "bad unit array");
   if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_SINGLE_READ)
     KVF_FAIL(KVF_EINVAL, "bad pack schedule %d", schedule);
-  if (slab_bytes < 0) KVF_FAIL(KVF_EINVAL, "negative slab_bytes");
-  std::vector<kvf_pack_unit> groups[17][4];
+  if (param < 0) KVF_FAIL(KVF_EINVAL, "negative schedule parameter");
+  const bool single = schedule == KVF_PACK_SINGLE_READ && phases == (1 | 2 | 4 | 8);
+  std::vector<kvf_pack_unit> by_dtype[4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
     if (st != KVF_OK) return st;
-    groups[pack_variant(units[k])][units[k].src.dtype].push_back(units[k]);
+    by_dtype[units[k].src.dtype].push_back(units[k]);
   }
-  // AUTO = the two-pass kernels: fastest measured on B200 so far
-  const bool single = schedule == KVF_PACK_SINGLE_READ && phases == (1 | 2 | 4 | 8);
+  std::vector<kvf_pack_unit> groups[17][4];
+  for (int dt = 0; dt < 4; ++dt) {
+    std::vector<kvf_pack_unit> rest;
+    if (single && dt != KVF_I8) {
+      kvf_status st = launch_single_read(by_dtype[dt], dt, param, s, &rest);
+      if (st != KVF_OK) return st;
+    } else {
+      rest.swap(by_dtype[dt]);
+    }
+    for (const auto& u : rest) groups[pack_variant(u)][dt].push_back(u);
+  }
   for (int v = 0; v <= 16; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        kvf_status st = (single && v != 0 && dt != KVF_I8)
-                            ? launch_single_read(groups[v][dt], v, dt, slab_bytes, s)
-                            : launch_phases(groups[v][dt], v, dt, phases, s);
+        kvf_status st = launch_phases(groups[v][dt], v, dt, phases, s);
         if (st != KVF_OK) return st;
       }
   return KVF_OK;
@@ -369,8 +375,8 @@ extern "C" kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units
 }
 
 extern "C" kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
-                                        int32_t schedule, int64_t slab_bytes, void* stream) {
-  return run(units, n_units, 1 | 2 | 4 | 8, schedule, slab_bytes,
+                                        int32_t schedule, int64_t param, void* stream) {
+  return run(units, n_units, 1 | 2 | 4 | 8, schedule, param,
              reinterpret_cast<cudaStream_t>(stream));
 }
 

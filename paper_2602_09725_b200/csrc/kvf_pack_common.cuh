@@ -186,6 +186,39 @@ __device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
 // when kRange, any |y| beyond the clip range) are redone exactly.  Without
 // kRange the caller guarantees |x| <= the group max the scale came from, which
 // bounds |y| <= 127 * (1 + 2^-22).
+// Fast path only; `bad` is set when the vector must be redone exactly.  The
+// rounding residual d is within 2^-16 of the exact one (reciprocal error
+// <= 2^-17 at |x/s| <= 128, plus at most one fp32 rounding of the product), so
+// only |d| > 1/2 - 2^-15 can round differently from the reference.
+template <bool kRange = true>
+__device__ __forceinline__ uint2 quantize8_fast(const float (&x)[8], float inv, bool& bad) {
+  const uint64_t kMagic2 = 0x4B4000004B400000ull;  // {1.5*2^23, 1.5*2^23}
+  const uint64_t inv2 = f2_pack(inv, inv);
+  uint32_t w[8];
+#pragma unroll
+  for (int e = 0; e < 8; e += 2) {
+    const uint64_t y = f2_mul(f2_pack(x[e], x[e + 1]), inv2);
+    const uint64_t rp = f2_add(y, kMagic2);
+    const uint64_t d = f2_sub(y, f2_sub(rp, kMagic2));
+    float d0, d1, y0, y1, r0, r1;
+    f2_unpack(d, d0, d1);
+    bad |= (fabsf(d0) > 0.499969482421875f) | (fabsf(d1) > 0.499969482421875f);
+    if constexpr (kRange) {
+      f2_unpack(y, y0, y1);
+      bad |= (fabsf(y0) > 127.25f) | (fabsf(y1) > 127.25f);
+    }
+    f2_unpack(rp, r0, r1);
+    w[e] = __float_as_uint(r0);
+    w[e + 1] = __float_as_uint(r1);
+  }
+  uint2 out;
+  out.x = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410) ^
+          0x80808080u;
+  out.y = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410) ^
+          0x80808080u;
+  return out;
+}
+
 template <bool kRange = true>
 __device__ __forceinline__ uint2 quantize8(const float (&x)[8], float s, float inv) {
   const uint64_t kMagic2 = 0x4B4000004B400000ull;  // {1.5*2^23, 1.5*2^23}

@@ -66,6 +66,18 @@ def test_assemble_disassemble_bit_exact(golden):
         assert np.array_equal(back.cpu().numpy(), t)
 
 
+# pack schedules (include/kvf.h kvf_pack_schedule): every one must give the
+# oracle's bytes; single_read with 16/8/2-CTA clusters as well as the default
+SCHEDULES = ["two_pass", "single_read", "single_read:8", "single_read:2", "auto"]
+
+
+def _pack(arr, n, mode):
+    name, _, param = mode.partition(":")
+    sched = {"auto": _lib.KVF_PACK_AUTO, "two_pass": _lib.KVF_PACK_TWO_PASS,
+             "single_read": _lib.KVF_PACK_SINGLE_READ}[name]
+    _lib.call("kvf_pack_batch_ex", arr, n, sched, int(param or 0), None)
+
+
 def _pack_unit(kv_dev, lay, res, T0, T, F, gs, frames, absmax, scales, triplet=0):
     """kvf_pack_unit for tokens [T0, T0+T) of layers 3*triplet.. of [T, L, H, D]."""
     H, D = lay[0], lay[1]
@@ -92,9 +104,8 @@ def _pack_unit(kv_dev, lay, res, T0, T, F, gs, frames, absmax, scales, triplet=0
 @pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
                                  (8, 128, 2, 4, 16, 8), (4, 64, 1, 4, 64, 1)])
 @pytest.mark.parametrize("res", ["R240", "R640", "R1080"])
-@pytest.mark.parametrize("mode", ["team", "twopass"])
-def test_fused_pack_matches_oracle(lay, res, mode, monkeypatch):
-    monkeypatch.setenv("KVF_PACK_MODE", mode)  # read by libkvf at each kvf_pack_batch
+@pytest.mark.parametrize("mode", SCHEDULES)
+def test_fused_pack_matches_oracle(lay, res, mode):
     H, D = lay[0], lay[1]
     T, Lyr, gs = 700, 5, 128 if D >= 128 else 64
     x = cases.to_bf16_values(ref.gen_synthetic_kv(T, Lyr, H, D, 0.9, 3, 0.3))
@@ -113,7 +124,7 @@ def test_fused_pack_matches_oracle(lay, res, mode, monkeypatch):
             outs.append((trip, T0, Tc, plan, fr, sc))
             scratch.append(am)  # descriptors hold raw pointers: keep the buffers alive
     arr = (_lib.kvf_pack_unit * len(units))(*units)
-    _lib.call("kvf_pack_batch", arr, len(units), None)
+    _pack(arr, len(units), mode)
     torch.cuda.synchronize()
     xp = ref.pad_layers(x)
     for trip, T0, Tc, plan, fr, sc in outs:
@@ -126,20 +137,21 @@ def test_fused_pack_matches_oracle(lay, res, mode, monkeypatch):
 
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("mode", ["team", "twopass"])
-def test_pack_paged_source_dtypes(dtype, mode, monkeypatch):
+@pytest.mark.parametrize("mode", SCHEDULES)
+def test_pack_paged_source_dtypes(dtype, mode):
     """Pack from a paged [blocks, 16, H, D] cache through a shuffled block table
-    (vLLM layout) for every source dtype; codes, scales, frames vs the oracle."""
-    monkeypatch.setenv("KVF_PACK_MODE", mode)
-    H, D, gs, bs, T, res = 8, 128, 128, 16, 1234, "R480"
+    (vLLM layout) for every source dtype, the chunk starting mid-block (token
+    base 5); codes, scales, frames vs the oracle."""
+    H, D, gs, bs, T, res, t0 = 8, 128, 128, 16, 1234, "R480", 5
     lay = (H, D, 1, H, 1, D)
     x = ref.gen_synthetic_kv(T, 3, H, D, 0.9, 11, 0.3)
     xt = torch.from_numpy(x).to(dtype)
     x = xt.float().numpy()                         # the values the kernel sees
-    nblk = (T + bs - 1) // bs
+    nblk = (T + t0 + bs - 1) // bs
     perm = torch.randperm(nblk + 7, generator=torch.Generator().manual_seed(5))[:nblk]
-    pool = torch.zeros((3, nblk + 7, bs, H, D), dtype=dtype)
-    tok = torch.arange(T)
+    # other tokens of the pool hold larger values: they must not enter the maxima
+    pool = torch.full((3, nblk + 7, bs, H, D), 1000.0).to(dtype)
+    tok = torch.arange(T) + t0
     for p in range(3):
         pool[p].view(-1, H, D)[perm[tok // bs] * bs + tok % bs] = xt[:, p]
     pool = pool.cuda()
@@ -158,13 +170,13 @@ def test_pack_paged_source_dtypes(dtype, mode, monkeypatch):
     u.src.block_stride = bs * H * D
     u.src.slot_stride = H * D
     u.src.head_stride = D
-    u.src.token_base = 0
+    u.src.token_base = t0
     u.plan = plan.to_c(gs)
     u.absmax = am.data_ptr()
     u.scales = sc.data_ptr()
     from paper_2602_09725_b200 import _dev
     u.frames = _dev.surface_of(fr)
-    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * 1)(u), 1, None)
+    _pack((_lib.kvf_pack_unit * 1)(u), 1, mode)
     torch.cuda.synchronize()
     v, s = ref.quantize(x, gs)
     want = ref.assemble_frames(v.reshape(T, 3, H * D), ref.Plan(T, res, *lay, F=4))
@@ -451,12 +463,11 @@ def test_wide_and_narrow_caches_pack_restore(H, D, gs):
             assert torch.equal(mem.read(t, p).cpu(), deq[t, p].reshape(-1))
 
 
-@pytest.mark.parametrize("mode", ["twopass", "team"])
-def test_tiny_and_ragged_units_pack_then_restore(mode, monkeypatch):
+@pytest.mark.parametrize("mode", SCHEDULES)
+def test_tiny_and_ragged_units_pack_then_restore(mode):
     """Units of 1..129 tokens (fewer tokens than F, partial last segments, one
     token) in ONE kvf_pack_batch, then the GPU frames restored to int8 slots in
     ONE restore batch: frames, scales and codes identical to the oracle."""
-    monkeypatch.setenv("KVF_PACK_MODE", mode)
     from paper_2602_09725_b200 import _dev
     specs = [(T, res, lay) for T in (1, 2, 3, 4, 5, 7, 15, 16, 17, 63, 64, 65, 129)
              for res, lay in (("R240", (8, 128, 1, 8, 1, 128)), ("R1080", (8, 128, 2, 4, 16, 8)))]
@@ -474,7 +485,7 @@ def test_tiny_and_ragged_units_pack_then_restore(mode, monkeypatch):
         units.append(u)
         keep += [kv, am]
         checks.append((T, lay, plan, v, s, want, fr, sc))
-    _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * len(units))(*units), len(units), None)
+    _pack((_lib.kvf_pack_unit * len(units))(*units), len(units), mode)
     torch.cuda.synchronize()
     r_units, outs = [], []
     for T, lay, plan, v, s, want, fr, sc in checks:

@@ -5,7 +5,7 @@ reference result, then times each schedule and checks that its frames and
 scales are bit-identical.  One JSON line per schedule.
 
     python tools/pack_sweep.py [--model llama3-8b --tokens 32768 --layout identity]
-                               [--slabs 8,16,24,32] [--steps 20]
+                               [--clusters 0,16,8] [--steps 20]
 """
 import argparse
 import json
@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=32768)
     ap.add_argument("--layout", default="identity")
     ap.add_argument("--res", default="R1080")
-    ap.add_argument("--slabs", default="8,16,24,32")
+    ap.add_argument("--clusters", default="0,16,8")
     ap.add_argument("--steps", type=int, default=20)
     a = ap.parse_args()
     args = argparse.Namespace(model=a.model, tokens=a.tokens, layout=a.layout, res=a.res, page=16,
@@ -45,9 +45,8 @@ def main():
     ref_frames = [f.clone() for f in w.frames]
     ref_scales = [x.clone() for x in w.scales]
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
-    for x in a.slabs.split(","):   # "MB" or "MB:lag:ra:rb" (tuning hook, low bits)
-        f = [int(v) for v in x.split(":")] + [0, 0, 0]
-        configs.append((_lib.KVF_PACK_SINGLE_READ, (f[0] << 20) | f[1] | (f[2] << 4) | (f[3] << 6)))
+    for x in a.clusters.split(","):   # CTAs per cluster, 0 = auto
+        configs.append((_lib.KVF_PACK_SINGLE_READ, int(x)))
     for sched, slab in configs:
         for f in w.frames:
             f.fill_(7)
@@ -70,7 +69,7 @@ def main():
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
         print(json.dumps({"schedule": "two_pass" if sched == 1 else "single_read",
-                          "slab_mb": slab >> 20, "lag": slab & 0xF, "ra": (slab >> 4) & 3, "rb": (slab >> 6) & 3, "ms_median": round(med, 4),
+                          "cluster": slab, "ms_median": round(med, 4),
                           "ms_min": round(per[0], 4), "achieved_gbs": round(ach, 1),
                           "frac": round(ach / 6558.7, 4), "bit_exact": ok,
                           "model": a.model, "tokens": a.tokens, "layout": a.layout}), flush=True)
