@@ -39,6 +39,9 @@ MODELS = {  # name -> (layers, kv heads, head dim)
 LAYOUTS = {  # name -> (a_h, b_h, a_d, b_d) as functions of (H, D)
     "identity": lambda H, D: (1, H, 1, D),
     "paper": lambda H, D: (H, 1, 1, D),
+    # tile rows narrower than 8 channels (shared-memory band kernels):
+    "col1": lambda H, D: (1, H, D, 1),            # (8,128,1,8,128,1): tile D x H
+    "a2b4": lambda H, D: (2, H // 2, D // 4, 4),  # (8,128,2,4,32,4): tile 64 x 16
 }
 CHUNK = 10_000  # fk/container.py:29 DEFAULT_CHUNK_TOKENS
 

@@ -19,6 +19,12 @@ namespace kvf {
 
 kvf_status launch_pack_cluster(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                                int64_t param, cudaStream_t s, bool* launched);
+bool pack_band_ok(const kvf_pack_unit& u);
+kvf_status launch_pack_band(const std::vector<kvf_pack_unit>& units, int32_t dtype,
+                            cudaStream_t s);
+// pack group variants: 0 generic, 1..16 fast kernels (VPL), kBandBase + v =
+// shared-memory band frames kernel with the absmax of variant v
+constexpr int kBandBase = 20;
 
 namespace {
 
@@ -155,17 +161,15 @@ __global__ void __launch_bounds__(kThreads)
 // ------------------------------------------------------------------- host
 bool aligned(const void* p, int64_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-int pack_variant(const kvf_pack_unit& u) {
+// VPL of the vectorised source kernels (absmax, frames) or 0: source-side
+// conditions only (the absmax ignores the tiling).
+int source_vpl(const kvf_pack_unit& u) {
   const kvf_plan& p = u.plan;
   int64_t C = (int64_t)p.H * p.D;
   if (C % 256 != 0) return 0;
   int vpl = (int)(C / 256);
   if (vpl != 1 && vpl != 2 && vpl != 4 && vpl != 8 && vpl != 16) return 0;
-  if (p.b_d % 8 != 0) return 0;
   if (u.src.dtype != KVF_I8 && p.group_size % 8 != 0) return 0;
-  if (!aligned(u.frames.base, 8) || u.frames.frame_stride % 8 || u.frames.plane_stride % 8 ||
-      u.frames.row_pitch % 8)
-    return 0;
   int64_t es = (int64_t)dtype_size(u.src.dtype);
   int64_t va = u.src.dtype == KVF_I8 ? 8 : 16;
   for (int l = 0; l < 3; ++l)
@@ -174,6 +178,15 @@ int pack_variant(const kvf_pack_unit& u) {
       (u.src.block_stride * es) % va)
     return 0;
   return vpl;
+}
+
+int pack_variant(const kvf_pack_unit& u) {
+  const kvf_plan& p = u.plan;
+  if (p.b_d % 8 != 0) return 0;
+  if (!aligned(u.frames.base, 8) || u.frames.frame_stride % 8 || u.frames.plane_stride % 8 ||
+      u.frames.row_pitch % 8)
+    return 0;
+  return source_vpl(u);
 }
 
 kvf_status check_unit(const kvf_pack_unit& u) {
@@ -231,8 +244,17 @@ PackParams* make_params(const std::vector<kvf_pack_unit>& units, size_t at, size
 }
 
 // phases: bit 0 = zero scratch, bit 1 = absmax, bit 2 = scales, bit 3 = frames.
-kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
+kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int variant, int32_t dtype,
                          int phases, cudaStream_t s) {
+  const bool band = variant >= kBandBase;
+  const int vpl = band ? variant - kBandBase : variant;
+  if (band && (phases & 8)) {
+    if (phases & 7) {
+      kvf_status st = launch_phases(units, vpl, dtype, phases & 7, s);
+      if (st != KVF_OK) return st;
+    }
+    return launch_pack_band(units, dtype, s);
+  }
   for (size_t at = 0; at < units.size(); at += kMaxPackUnits) {
     size_t n = std::min<size_t>(kMaxPackUnits, units.size() - at);
     PackParams* P = make_params(units, at, n);
@@ -325,7 +347,7 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t 
     if (st != KVF_OK) return st;
     by_dtype[units[k].src.dtype].push_back(units[k]);
   }
-  std::vector<kvf_pack_unit> groups[17][4];
+  std::vector<kvf_pack_unit> groups[kBandBase + 17][4];
   for (int dt = 0; dt < 4; ++dt) {
     std::vector<kvf_pack_unit> rest;
     if (single && dt != KVF_I8) {
@@ -334,9 +356,13 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t 
     } else {
       rest.swap(by_dtype[dt]);
     }
-    for (const auto& u : rest) groups[pack_variant(u)][dt].push_back(u);
+    for (const auto& u : rest) {
+      int v = pack_variant(u);
+      if (v == 0 && pack_band_ok(u)) v = kBandBase + source_vpl(u);  // narrow tile rows
+      groups[v][dt].push_back(u);
+    }
   }
-  for (int v = 0; v <= 16; ++v)
+  for (int v = 0; v < kBandBase + 17; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
         kvf_status st = launch_phases(groups[v][dt], v, dt, phases, s);

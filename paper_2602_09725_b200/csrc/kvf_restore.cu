@@ -20,6 +20,11 @@
 #include "kvf_common.cuh"
 
 namespace kvf {
+
+bool restore_band_ok(const kvf_restore_unit& u);
+kvf_status launch_restore_band(const std::vector<kvf_restore_unit>& units, int32_t dtype,
+                               cudaStream_t s);
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -281,19 +286,24 @@ extern "C" kvf_status kvf_restore_batch(const kvf_restore_unit* units,
                                         int32_t n_units, void* stream) {
   if (n_units < 0 || (n_units > 0 && units == nullptr))
     KVF_FAIL(KVF_EINVAL, "bad unit array");
-  // Group by (variant, dtype) so each launch instantiates one kernel.
-  std::vector<kvf_restore_unit> groups[17][4];
+  // Group by (variant, dtype) so each launch instantiates one kernel; variant
+  // 17 = shared-memory band transpose (tile rows narrower than 8 channels).
+  constexpr int kBand = 17;
+  std::vector<kvf_restore_unit> groups[kBand + 1][4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
     if (st != KVF_OK) return st;
     if (units[k].n_frames == 0) continue;
-    groups[restore_variant(units[k])][units[k].dst.dtype].push_back(units[k]);
+    int v = restore_variant(units[k]);
+    if (v == 0 && restore_band_ok(units[k])) v = kBand;
+    groups[v][units[k].dst.dtype].push_back(units[k]);
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  for (int v = 0; v <= 16; ++v)
+  for (int v = 0; v <= kBand; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        kvf_status st = launch_group(groups[v][dt], v, dt, s);
+        kvf_status st = v == kBand ? launch_restore_band(groups[v][dt], dt, s)
+                                   : launch_group(groups[v][dt], v, dt, s);
         if (st != KVF_OK) return st;
       }
   return KVF_OK;

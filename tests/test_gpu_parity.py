@@ -546,3 +546,72 @@ def test_pack_frames_batch_with_supplied_maxima():
                                         ref.Plan(T, res, *lay, F=4))
             assert np.array_equal(sc.cpu().numpy(), s2)
             assert np.array_equal(fr.cpu().numpy(), want2)
+
+
+# ------------------------------------------- every tiling of 8 x 128 (b_d < 8 too)
+def _tilings_8x128():
+    return [(8, 128, c.a_h, c.b_h, c.a_d, c.b_d) for c in L.tiling_candidates(8, 128)]
+
+
+@pytest.mark.parametrize("res", ["R240", "R1080"])
+def test_every_tiling_pack_and_restore_match_oracle(res):
+    """All 32 tilings of H=8, D=128 (fk/layout.py:94-106), including the 12
+    whose tile rows are narrower than 8 channels (shared-memory band kernels):
+    pack (every schedule) gives the oracle's frames and scales, restore of the
+    oracle's frames gives its int8 codes and bf16 dequantised values, in ONE
+    batched call each for all tilings."""
+    from paper_2602_09725_b200 import _dev
+    T, H, D, gs = 150, 8, 128, 128
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, 3, H, D, 0.9, 21, 0.3))
+    kv = np_bf16_from_f32(x).cuda()
+    v, s = ref.quantize(x, gs)
+    deq = ref.dequantize(v, s, gs).reshape(T, 3, H * D)
+    lays = _tilings_8x128()
+    assert len(lays) == 32 and sum(l[5] < 8 for l in lays) == 12
+    wants = [ref.assemble_frames(v.reshape(T, 3, H * D), ref.Plan(T, res, *lay, F=4))
+             for lay in lays]
+    for mode in SCHEDULES:
+        units, keep, outs = [], [], []
+        for lay in lays:
+            plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+            fr = torch.full(plan.frame_shape(), 7, dtype=torch.uint8, device="cuda")
+            am = torch.zeros(_lib.load().kvf_pack_scratch_words(plan.to_c(gs)),
+                             dtype=torch.int32, device="cuda")
+            sc = torch.empty((3, H * D // gs), dtype=torch.float32, device="cuda")
+            u, _ = _pack_unit(kv, lay, res, 0, T, 4, gs, fr, am, sc)
+            units.append(u)
+            keep += [am]
+            outs.append((fr, sc))
+        _pack((_lib.kvf_pack_unit * len(units))(*units), len(units), mode)
+        torch.cuda.synchronize()
+        for lay, want, (fr, sc) in zip(lays, wants, outs):
+            np.testing.assert_array_equal(sc.cpu().numpy(), s, err_msg=f"{mode} {lay}")
+            np.testing.assert_array_equal(fr.cpu().numpy(), want, err_msg=f"{mode} {lay}")
+    for dtype in (torch.int8, torch.bfloat16):
+        caches, r_units, keep = [], [], []
+        for lay, want in zip(lays, wants):
+            plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+            fr = torch.from_numpy(want).cuda()
+            cache = torch.zeros((3, T, H, D), dtype=dtype, device="cuda")
+            dst = _lib.kvf_paged()
+            for p in range(3):
+                dst.layer[p] = cache[p].data_ptr()
+            dst.block_table = None
+            dst.block_size = 1
+            dst.dtype = _lib.KVF_I8 if dtype == torch.int8 else _lib.KVF_BF16
+            dst.block_stride = dst.slot_stride = H * D
+            dst.head_stride = D
+            dst.token_base = 0
+            sc = torch.from_numpy(s).cuda()
+            r_units.append(make_restore_unit(fr, plan, sc, dst, gs))
+            keep += [fr, sc]
+            caches.append(cache)
+        _lib.call("kvf_restore_batch", (_lib.kvf_restore_unit * len(r_units))(*r_units),
+                  len(r_units), None)
+        torch.cuda.synchronize()
+        for lay, cache in zip(lays, caches):
+            got = cache.permute(1, 0, 2, 3).reshape(T, 3, H * D).cpu()
+            if dtype == torch.int8:
+                np.testing.assert_array_equal(got.numpy(), v.reshape(T, 3, H * D), err_msg=str(lay))
+            else:
+                assert torch.equal(got, torch.from_numpy(deq).to(torch.bfloat16)), lay
