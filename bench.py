@@ -57,15 +57,17 @@ def parse():
     ap.add_argument("--layout", default="identity", choices=sorted(LAYOUTS))
     ap.add_argument("--res", default="R1080")
     ap.add_argument("--page", type=int, default=16)
-    ap.add_argument("--requests", type=int, default=0,
-                    help="contexts in the job (default: one per GPU -> weak scaling)")
-    ap.add_argument("--shard", default="layer", choices=["balanced", "layer", "chunk"],
+    ap.add_argument("--requests", type=int, default=1,
+                    help="contexts in the job: 1 (default) = one context split over the "
+                         "GPUs (strong scaling); 0 = one context per GPU (weak scaling)")
+    ap.add_argument("--shard", default="balanced", choices=["balanced", "layer", "chunk"],
                     help="unit -> GPU assignment policy (paper_2602_09725_b200/shard.py)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fetch", action="store_true", help="skip the fetch-to-ready leg")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
-    ap.add_argument("--cpu-units", type=int, default=2, help="sample units per CPU worker")
+    ap.add_argument("--cpu-tokens", type=int, default=2000,
+                    help="tokens of the sample unit each CPU worker restores per step")
     return ap.parse_args()
 
 
@@ -449,9 +451,11 @@ def ctypes_copy(dst, src):
     ctypes.memmove(ctypes.addressof(dst), ctypes.addressof(src), ctypes.sizeof(src))
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary
-    (profiles/<round>/ncu_traffic.json, written by tools/ncu_summary.py), or None."""
+def ncu_traffic(kernel: str, config_key: str):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
+    of THIS configuration (profiles/<round>/ncu_traffic.json, written by
+    tools/ncu_summary.py with the bench config key), or None: a profile of
+    another configuration is not this run's traffic."""
     import glob
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")),
                        reverse=True):
@@ -460,10 +464,56 @@ def ncu_traffic(kernel: str):
                 rec = json.load(fh).get(kernel)
         except (OSError, ValueError):
             continue
-        if rec:
+        if rec and rec.get("config") == config_key:
             return {"bytes_per_launch": rec["dram_bytes_per_launch"],
                     "source": os.path.relpath(path, ROOT) + " (" + rec["report"] + ")"}
     return None
+
+
+def config_key(args, world):
+    return (f"{args.model}/{args.tokens}/{args.layout}/{args.res}/page{args.page}/"
+            f"req{args.requests}/{args.shard}/n{world}")
+
+
+def count_launches(fn, stream, torch):
+    """Kernel launches of ONE step, observed with the CUDA activity profiler
+    (CUPTI) on an extra, untimed step: {kernel name: count}, or None."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn(stream)
+            torch.cuda.synchronize()
+        out = {}
+        for e in prof.events():
+            if getattr(e, "device_type", None) is not None and "CUDA" in str(e.device_type):
+                out[e.name] = out.get(e.name, 0) + 1
+        return out or None
+    except Exception:  # profiler unavailable: reported as unobserved
+        return None
+
+
+def oracle_unit_check(w, torch):
+    """Every slot of one full reference chunk (unit 0: 10,000 tokens x its real
+    layers) against the CPU oracle: quantize (fk/kvmodel.py:127-144) ->
+    dequantize (fk/kvmodel.py:147-152) -> bf16 RNE, vs the restored paged
+    cache read through the block table.  Returns (slots, mismatching slots)."""
+    from oracle import ref
+    u = w.mine[0]
+    k = sorted({(x.request, x.kv, x.triplet) for x in w.mine}).index((u.request, u.kv, u.triplet))
+    slab, cache = w.slabs[k], w.caches[k]
+    t0, tc, real = u.token_start, u.tokens, u.real_layers
+    x = slab[t0:t0 + tc].float().cpu().numpy()                      # [tc, real, H, D]
+    xp = np.zeros((tc, 3, w.H, w.D), np.float32)
+    xp[:, :real] = x
+    v, s = ref.quantize(xp, 128)
+    want = torch.from_numpy(ref.dequantize(v, s, 128)).to(torch.bfloat16)[:, :real]
+    toks = torch.arange(t0, t0 + tc)
+    blk = w.table.cpu()[toks // w.page].long()
+    got = torch.stack([cache[p][blk.to(cache.device), (toks % w.page).to(cache.device)].cpu()
+                       for p in range(real)], dim=1)                  # [tc, real, H, D]
+    bad = (got.view(torch.int16) != want.view(torch.int16)).reshape(tc, real, -1).any(-1)
+    return int(tc * real), int(bad.sum())
 
 
 def load_peaks():
@@ -475,37 +525,70 @@ def load_peaks():
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU restore path (oracle port) on host cores."""
+    """--impl reference: the reference's own restore code (vendored framekv,
+    oracle/bench_ref.py) on all host cores; rank 0 only."""
     if rank != 0:
         return
-    from oracle import bench_cpu
+    from oracle import bench_ref
     Lyr, H, D = MODELS[args.model]
     lay = (H, D) + LAYOUTS[args.layout](H, D)
-    times = []
-    for k in range(args.warmup + args.steps):
-        elems, wall, cores = bench_cpu.run("restore", units_per_worker=1, T=CHUNK, H=H, D=D,
-                                           res=args.res, lay=lay)
-        if k >= args.warmup:
-            times.append((elems, wall))
-    elems = sum(e for e, _ in times)
-    wall = sum(t for _, t in times)
+    if not bench_ref.available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/framekv_ref not vendored"}), flush=True)
+        return
+    single = cpu_reference(args, H, D, lay, workers=1, steps=3)
+    r = bench_ref.RefRestore(T=args.cpu_tokens, H=H, D=D, res=args.res, lay=lay)
+    for _ in range(args.warmup):
+        r.step()
+    elems = wall = 0.0
+    for _ in range(args.steps):
+        e, t = r.step()
+        elems += e
+        wall += t
+    r.close()
     gbs = 2.0 * elems / wall / 1e9
+    cores = r.workers
     line = {
         "metric": "KV restore GB/s (frames->bf16 paged KV), 32K ctx", "impl": "reference",
         "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(1e3 * wall / len(times), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16",
-        "data": "synthetic", "config": workload_config(args, world),
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} processes x 1 unit of {CHUNK} tokens x 3 layers "
-                                   f"({args.model} shape, {args.layout}, {args.res}) per step"},
+        "warmup": args.warmup, "ms_per_step": round(1e3 * wall / args.steps, 3),
+        "higher_is_better": True, "scaling": scaling_kind(args), "vs_baseline": None,
+        "dtype": "u8->bf16", "data": "synthetic", "config": workload_config(args, world),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores,
+                         "kind": "reference", "cpu_model": bench_ref.cpu_model(),
+                         "sample": f"{cores} processes x 1 unit of {args.cpu_tokens} tokens x 3 "
+                                   f"layers ({args.model} shape, {args.layout}, {args.res}) per "
+                                   f"step: reference disassemble_frames + dequantize + bf16 + "
+                                   f"PagedMemory.page_write (vendored framekv)",
+                         "single_process": single},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, world=1):
+def cpu_reference(args, H, D, lay, workers=None, steps=5):
+    """The reference restore on `workers` processes (None = all cores)."""
+    from oracle import bench_ref
+    r = bench_ref.RefRestore(workers=workers, T=args.cpu_tokens, H=H, D=D, res=args.res, lay=lay)
+    elems = wall = 0.0
+    for _ in range(steps):
+        e, t = r.step()
+        elems += e
+        wall += t
+    r.close()
+    return {"value": round(2.0 * elems / wall / 1e9, 4), "unit": "GB/s", "cores": r.workers,
+            "kind": "reference", "cpu_model": bench_ref.cpu_model(),
+            "sample": f"{r.workers} process(es) x {steps} steps x 1 unit of {args.cpu_tokens} "
+                      f"tokens x 3 layers: reference disassemble_frames + dequantize + bf16 + "
+                      f"PagedMemory.page_write (vendored framekv, oracle/bench_ref.py)"}
+
+
+def scaling_kind(args):
+    return "weak" if args.requests == 0 else "strong"
+
+
+def workload_config(args, world=1, l2=None):
     Lyr, H, D = MODELS[args.model]
     req = args.requests or world
     return {"workload": f"{req} x {args.model}-shaped K+V context(s), {args.tokens} tokens, "
@@ -516,7 +599,7 @@ def workload_config(args, world=1):
             "group_size": 128, "F": 4, "block_size": args.page,
             "parallelism": f"dp{world}: (request, K/V, triplet, chunk) units sharded "
                            f"'{args.shard}' across GPUs, no data-path collective",
-            "l2": "inputs larger than L2 (2.3 GB frames in + 4.3 GB out per GPU per step)"}
+            "l2": l2}
 
 
 def main():
@@ -562,6 +645,19 @@ def main():
     pack_ach = 3.0 * w.elems / (pack_ms * 1e-3) / 1e9
 
     chk_slots, chk_bad = w.check_restored()   # after the timed restores, outside timing
+    orc_slots, orc_bad = oracle_unit_check(w, torch) if rank == 0 else (0, 0)
+    launches = count_launches(w.restore, stream, torch)
+    units_per_rank = [len(w.units)]
+    if d is not None:
+        units_per_rank = [None] * world
+        d.all_gather_object(units_per_rank, len(w.units))
+    props = torch.cuda.get_device_properties(dev)
+    l2 = {"l2_bytes": int(getattr(props, "L2_cache_size", 0)),
+          "frames_in_per_step_bytes": int(w.frame_bytes), "kv_out_per_step_bytes": 2 * w.elems,
+          "inputs_exceed_l2": bool(w.frame_bytes > getattr(props, "L2_cache_size", 0)),
+          "note": "per GPU; no L2 flush between steps: inputs exceed L2"
+                  if w.frame_bytes > getattr(props, "L2_cache_size", 0) else
+                  "per GPU; inputs fit in L2 (no flush between steps)"}
     e2e = None
     if not args.no_e2e:
         e2e_ms, h2d, d2h = e2e_restore(w, max(3, args.steps // 4), torch)
@@ -582,15 +678,12 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        from oracle import bench_cpu
+        from oracle import bench_cpu, bench_ref
         Lyr, H, D = MODELS[args.model]
         lay = (H, D) + LAYOUTS[args.layout](H, D)
-        elems, wall, cores = bench_cpu.run("restore", units_per_worker=args.cpu_units, T=CHUNK,
-                                           H=H, D=D, res=args.res, lay=lay)
-        cpu = {"value": round(2.0 * elems / wall / 1e9, 4), "unit": "GB/s", "cores": cores,
-               "kind": "port",
-               "sample": f"{cores} processes x {args.cpu_units} units of {CHUNK} tokens x 3 "
-                         f"layers: oracle disassemble_frames + dequantize + bf16 + paged scatter"}
+        if bench_ref.available():
+            cpu = cpu_reference(args, H, D, lay, steps=5)
+            cpu["single_process"] = cpu_reference(args, H, D, lay, workers=1, steps=2)
         if fetch is not None:  # the same host's cores decoding the context's KVFC streams
             sym, dwall, dcores = bench_cpu.run("decode", units_per_worker=1, T=CHUNK, H=H, D=D,
                                                res=args.res, lay=lay)
@@ -605,27 +698,39 @@ def main():
         clocks = clk.summary()
         # one restore launch per step covers all 88 units: per-launch traffic
         # compares with algorithmic_bytes_per_step (multi-GPU: per rank)
-        traffic = ncu_traffic("restore_fast_kernel")
+        rkernel = "restore_band_kernel" if LAYOUTS[args.layout](w.H, w.D)[3] < 8 \
+            else "restore_fast_kernel"
+        traffic = ncu_traffic(rkernel, config_key(args, world))
         line = {
             "metric": "KV restore GB/s (frames->bf16 paged KV), 32K ctx",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8->bf16", "data": "synthetic",
-            "config": workload_config(args, world),
+            "scaling": scaling_kind(args), "vs_baseline": None, "dtype": "u8->bf16",
+            "data": "synthetic", "config": workload_config(args, world, l2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic and traffic["bytes_per_launch"],
-                         "traffic_source": traffic and traffic["source"],
+                         "traffic_source": traffic["source"] if traffic else
+                         "no ncu capture of this configuration committed",
                          "peak_kind": peak_kind,
-                         "kernel": "restore_fast_kernel (kvf_restore_batch)",
+                         "kernel": f"{rkernel} (kvf_restore_batch)",
                          "algorithmic_bytes_per_step": 3 * w.elems},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "fetch_to_ready": fetch,
-            "gpu_launches": w.n_launch_restore * args.steps,
-            "restore_check": {"slots": chk_slots, "mismatch": chk_bad,
-                              "against": "kvf_quantize of each unit's token chunk, "
-                                         "dequantised and rounded to bf16 (sampled slots)"},
+            "gpu_launches": (sum(launches.values()) * args.steps if launches
+                             else w.n_launch_restore * args.steps),
+            "gpu_launches_source": ({"per_step": launches, "how": "CUDA activity profiler "
+                                     "(CUPTI) over one extra untimed step, x steps"}
+                                    if launches else "computed (profiler unavailable)"),
+            "restore_check": {
+                "oracle_unit": {"slots": orc_slots, "mismatch": orc_bad,
+                                "against": "oracle quantize -> dequantize -> bf16 of every slot "
+                                           "of unit 0 (one full 10,000-token chunk), read back "
+                                           "through the block table"},
+                "sampled": {"slots": chk_slots, "mismatch": chk_bad,
+                            "against": "kvf_quantize of each unit's token chunk, dequantised "
+                                       "and rounded to bf16 (16 sampled tokens per unit)"}},
             "clocks": clocks,
             "pack": {"ms_per_step": round(pack_ms, 4),
                      "achieved_gbs": round(pack_ach, 1), "frac": round(pack_ach / peak, 4),
@@ -637,7 +742,7 @@ def main():
                                  "maxima supplied (single read); the reference computes them, "
                                  "which is the two-pass figure above"}},
             "step_ms_min_max": [round(min(per), 4), round(max(per), 4)],
-            "units": w.all_units, "units_rank0": len(w.units), "elems_rank0": w.elems,
+            "units": w.all_units, "units_per_rank": units_per_rank, "elems_rank0": w.elems,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

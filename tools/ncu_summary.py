@@ -1,6 +1,10 @@
 """Summarise ncu output (read here, no GPU needed) into profiles/<round>/.
 
-    python tools/ncu_summary.py r01 gpurun_out/launches.csv gpurun_out/prof_*.ncu-rep
+    python tools/ncu_summary.py r01 [--config KEY] gpurun_out/launches.csv gpurun_out/prof_*.ncu-rep
+
+--config KEY tags the ncu_traffic.json entries with the bench configuration the
+captures ran (bench.config_key: model/tokens/layout/res/page/requests/shard/n);
+bench.py only reports roofline.traffic from a capture of its own configuration.
 
 Writes launches.md (per-kernel launch-time shares of the serialized launch
 list) and <kernel>.md (key raw metrics + top warp-stall reasons) per report.
@@ -46,7 +50,7 @@ def launches(path, out):
                      f"{sum(v) / 1e6:.3f} | {sum(v) / total * 100:.1f}% |\n")
 
 
-def report(path, out):
+def report(path, out, config=None):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -71,6 +75,7 @@ def report(path, out):
             data = json.load(open(tj)) if os.path.exists(tj) else {}
             short = name.split("(")[0].split("::")[-1].split("<")[0]
             data[short] = {"dram_bytes_per_launch": traffic * 1e9, "report": os.path.basename(path),
+                           "config": config,
                            "duration": vals[h.index("gpu__time_duration.sum")] + " "
                            + units[h.index("gpu__time_duration.sum")]}
             json.dump(data, open(tj, "w"), indent=1, sort_keys=True)
@@ -90,12 +95,15 @@ def main():
     rnd = sys.argv[1]
     out_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", rnd)
     os.makedirs(out_dir, exist_ok=True)
-    for p in sys.argv[2:]:
+    args, config = sys.argv[2:], None
+    if args and args[0] == "--config":
+        config, args = args[1], args[2:]
+    for p in args:
         base = os.path.basename(p)
         if p.endswith(".csv"):
             launches(p, os.path.join(out_dir, base.replace(".csv", ".md")))
         elif p.endswith(".ncu-rep"):
-            report(p, os.path.join(out_dir, base.replace(".ncu-rep", ".md")))
+            report(p, os.path.join(out_dir, base.replace(".ncu-rep", ".md")), config)
 
 
 if __name__ == "__main__":
