@@ -20,6 +20,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context: see paper_2602_09725_b200.use_fetch_hw_queues
 import statistics
 import subprocess
 import sys

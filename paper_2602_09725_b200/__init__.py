@@ -22,10 +22,18 @@ __version__ = "0.1.0"
 
 import os as _os
 
-# The decode pipeline runs each part and each in-flight fetch batch on its own
-# CUDA stream.  With the driver's default 8 hardware connections those streams
-# share queues, and a long (R1080) range decode then blocks unrelated kernels
-# behind it: measured on B200, an unthrottled C5 fetch at R1080 takes 0.29 s
-# with 8 connections and 0.13 s with 32.  Takes effect only if set before the
-# process creates its CUDA context; an explicit user setting wins.
-_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+def use_fetch_hw_queues(n: int = 32) -> bool:
+    """Ask the CUDA driver for ``n`` hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS).
+
+    The decode pipeline runs each part and each in-flight fetch batch on its own
+    CUDA stream.  With the driver's default 8 hardware connections those streams
+    share queues, and a long (R1080) range decode then blocks unrelated kernels
+    behind it: measured on B200, an unthrottled C5 fetch at R1080 takes 0.29 s
+    with 8 connections and 0.13 s with 32.  The setting is process-wide and only
+    takes effect before the process creates its CUDA context, so importing this
+    package does NOT change it: call this first (bench.py and tools/ do), or
+    export the variable.  An explicit user setting wins.  Returns True when the
+    value in effect is ``n``."""
+    _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", str(n))
+    return _os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] == str(n)

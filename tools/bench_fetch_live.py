@@ -22,6 +22,7 @@ import gc
 import json
 import multiprocessing as mp
 import os
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context: see paper_2602_09725_b200.use_fetch_hw_queues
 import shutil
 import sys
 import tempfile

@@ -1,5 +1,6 @@
 """GPU: time decode_batch host prep vs device work for C2-sized unit sets (R1080/R240)."""
 import os
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context: see paper_2602_09725_b200.use_fetch_hw_queues
 import sys
 import time
 

@@ -4,6 +4,7 @@ per-activity start/end relative to the first, to see copy/decode overlap.
     python tools/timeline_decode.py R240
 """
 import os
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # before any CUDA context: see paper_2602_09725_b200.use_fetch_hw_queues
 import sys
 
 import torch
