@@ -144,7 +144,7 @@ def full_check(mems, qs, Lyr, T):
     return bad
 
 
-def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
+def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link, pass_no=0):
     recs = tl.records
     first = min(r["transfer_start"] for r in recs)
     last_rx = max(r["transfer_end"] for r in recs)
@@ -174,9 +174,22 @@ def emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, link):
         "batches": [(round(r["decode_start"], 4), round(r["decode_end"], 4), r.get("batch"),
                      round(r.get("host_decode_s", 0), 4), round(r.get("host_restore_s", 0), 4))
                     for r in {r["decode_start"]: r for r in recs}.values()] if args.verbose else None,
-        "setup_pack_s": round(setup_s, 1),
+        "setup_pack_s": round(setup_s, 1), "pass": pass_no,
     }
     print(json.dumps(line), flush=True)
+    return line
+
+
+def summarize(lines, res, rate):
+    import statistics
+    r = sorted(x["ready_s"] for x in lines)
+    p95 = r[min(len(r) - 1, int(round(0.95 * (len(r) - 1))))]
+    print(json.dumps({"summary": True, "resolution": res, "rate_gbps": rate, "passes": len(r),
+                      "ready_p50_s": round(statistics.median(r), 4), "ready_p95_s": round(p95, 4),
+                      "ready_min_s": r[0], "ready_max_s": r[-1],
+                      "p95_over_p50": round(p95 / statistics.median(r), 3),
+                      "link_s_at_rate": lines[0]["link_s_at_rate"],
+                      "mismatch": sum(x["sampled_slots_mismatch"] for x in lines)}), flush=True)
 
 
 def main():
@@ -188,6 +201,8 @@ def main():
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--verbose", action="store_true", help="per-batch timings in each line")
     ap.add_argument("--full-check", action="store_true", help="compare every slot, not a sample")
+    ap.add_argument("--passes", type=int, default=1,
+                    help="timed passes per (class, rate); > 1 adds a p50/p95 summary line")
     ap.add_argument("--link", default="model", choices=["model", "tcp"],
                     help="model: constant-rate arrival replay; tcp: live loopback server")
     args = ap.parse_args()
@@ -219,15 +234,21 @@ def main():
                                    fetch_fn=link)
             del link
         for rate in [float(r) for r in args.rates.split(",")] if args.link == "model" else []:
-            link = ModelLink(store, rate)
-            link.stage(chunks, codes)
-            mems = new_mems(qs, args.tokens, Lyr, H, D)
-            gc.collect()   # no collector pause inside the timed fetch
-            torch.cuda.synchronize()
-            tl = FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=rate or 400.0, mem=mems,
-                                        real_layers=Lyr, fetch_fn=link, workers=args.workers)
-            emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s, "modelled constant-rate link")
-            del mems, link
+            lines = []
+            for k in range(args.passes):
+                link = ModelLink(store, rate)
+                link.stage(chunks, codes)
+                mems = new_mems(qs, args.tokens, Lyr, H, D)
+                gc.collect()   # no collector pause inside the timed fetch
+                torch.cuda.synchronize()
+                tl = FE.live_fetch_pipeline(None, chunks, None, policy, prior_gbps=rate or 400.0,
+                                            mem=mems, real_layers=Lyr, fetch_fn=link,
+                                            workers=args.workers)
+                lines.append(emit(tl, res, rate, coded, mems, qs, Lyr, args, setup_s,
+                                  "modelled constant-rate link", k))
+                del mems, link
+            if args.passes > 1:
+                summarize(lines, res, rate)
         for rate in [float(r) for r in args.rates.split(",")] if args.link == "tcp" else []:
             # the chunk server runs in its own process (a remote node's role):
             # it does not share this process's GIL with the fetcher
