@@ -133,7 +133,8 @@ typedef struct kvf_pack_unit {
   kvf_paged src;           /* bf16/f16/f32 KV to quantize, or int8 codes */
   kvf_plan plan;
   uint32_t* absmax;        /* device scratch of kvf_pack_scratch_words(&plan) u32:
-                              [3, G] |x| maxima (f32 bit patterns) + [3, G] reserved */
+                              [3, G] |x| maxima (f32 bit patterns), then schedule
+                              scratch */
   float* scales;           /* device [3, G] out (ignored for int8 sources) */
   kvf_surface frames;      /* out: frame_count frames */
 } kvf_pack_unit;
@@ -194,9 +195,13 @@ kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
 typedef enum kvf_pack_schedule {
   KVF_PACK_AUTO = 0,        /* the fastest measured on this build */
   KVF_PACK_TWO_PASS = 1,    /* absmax kernel, then frames kernel: reads the source twice */
-  KVF_PACK_SINGLE_READ = 2  /* thread-block clusters, one per (unit, plane, group) at a
+  KVF_PACK_SINGLE_READ = 2, /* thread-block clusters, one per (unit, plane, group) at a
                                time, exchange the all-token maxima through distributed
                                shared memory; the quantising re-read is an L2 hit */
+  KVF_PACK_STREAM = 3       /* one HBM read: clusters of 16 (or 8) CTAs own whole
+                               (unit, plane, group) sub-units, stream them through
+                               shared memory with TMA, exchange the maxima through
+                               distributed shared memory and re-read from L2 */
 } kvf_pack_schedule;
 
 /* kvf_pack_batch with an explicit schedule.  `param` (single read only): bits

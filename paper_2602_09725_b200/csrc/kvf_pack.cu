@@ -19,6 +19,9 @@ namespace kvf {
 
 kvf_status launch_pack_cluster(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                                int64_t param, cudaStream_t s, bool* launched);
+kvf_status launch_pack_stream(const std::vector<kvf_pack_unit>& units, int32_t dtype,
+                              int cluster, int probe, cudaStream_t s,
+                              std::vector<kvf_pack_unit>* rest);
 bool pack_band_ok(const kvf_pack_unit& u);
 kvf_status launch_pack_band(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                             cudaStream_t s);
@@ -337,10 +340,12 @@ kvf_status launch_single_read(const std::vector<kvf_pack_unit>& units, int32_t d
 kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t schedule,
                int64_t param, cudaStream_t s) {
   if (n_units < 0 || (n_units > 0 && units == nullptr)) KVF_FAIL(KVF_EINVAL, "bad unit array");
-  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_SINGLE_READ)
+  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_STREAM)
     KVF_FAIL(KVF_EINVAL, "bad pack schedule %d", schedule);
   if (param < 0) KVF_FAIL(KVF_EINVAL, "negative schedule parameter");
-  const bool single = schedule == KVF_PACK_SINGLE_READ && phases == (1 | 2 | 4 | 8);
+  const bool all = phases == (1 | 2 | 4 | 8);
+  const bool single = schedule == KVF_PACK_SINGLE_READ && all;
+  const bool stream = schedule == KVF_PACK_STREAM && all;
   std::vector<kvf_pack_unit> by_dtype[4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
@@ -352,6 +357,10 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t 
     std::vector<kvf_pack_unit> rest;
     if (single && dt != KVF_I8) {
       kvf_status st = launch_single_read(by_dtype[dt], dt, param, s, &rest);
+      if (st != KVF_OK) return st;
+    } else if (stream && dt != KVF_I8) {
+      kvf_status st = launch_pack_stream(by_dtype[dt], dt, (int)(param & 0xFF),
+                                         (int)((param >> 8) & 0xFF), s, &rest);
       if (st != KVF_OK) return st;
     } else {
       rest.swap(by_dtype[dt]);

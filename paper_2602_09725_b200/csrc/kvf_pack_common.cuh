@@ -16,8 +16,7 @@ constexpr int kPackWarps = kPackThreads / 32;
 constexpr int kMaxPackUnits = 96;  // descriptors per launch (kernel params <= 32 KB)
 
 // Scratch words of a unit (kvf_pack_scratch_words): [3, G] |x| maxima (f32
-// bit patterns) | [3, G] words of step counters (the single-read kernel keeps
-// one counter per slab in the first word of its first (unit, plane)).
+// bit patterns) | [3, G] counter words.
 inline int64_t pack_scratch_words(const kvf_plan& p) {
   const int64_t G = (int64_t)p.H * p.D / p.group_size;
   return 6 * G;
@@ -43,7 +42,7 @@ inline PackUnitDev make_pack_unit_dev(const kvf_pack_unit& u) {
   d.G = (u.plan.H * u.plan.D) / u.plan.group_size;
   d.absmax = u.absmax;
   d.counters = u.absmax ? u.absmax + 3 * d.G : nullptr;
-  d.n_scratch = (int32_t)pack_scratch_words(u.plan);
+  d.n_scratch = 6 * d.G;  // the phase-split kernels use maxima + counters only
   d.scales = u.scales;
   d.fr = u.frames;
   d.div_bs = make_fastdiv(u.src.block_size);

@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=32768)
     ap.add_argument("--layout", default="identity")
     ap.add_argument("--res", default="R1080")
-    ap.add_argument("--clusters", default="0,16,8")
+    ap.add_argument("--clusters", default="")
+    ap.add_argument("--schedules", default="stream", help="comma list of stream / auto")
     ap.add_argument("--steps", type=int, default=20)
     a = ap.parse_args()
     args = argparse.Namespace(model=a.model, tokens=a.tokens, layout=a.layout, res=a.res, page=16,
@@ -45,8 +46,12 @@ def main():
     ref_frames = [f.clone() for f in w.frames]
     ref_scales = [x.clone() for x in w.scales]
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
-    for x in a.clusters.split(","):   # CTAs per cluster, 0 = auto
+    for x in filter(None, a.clusters.split(",")):   # CTAs per cluster, 0 = auto
         configs.append((_lib.KVF_PACK_SINGLE_READ, int(x)))
+    names = {"stream": _lib.KVF_PACK_STREAM, "auto": _lib.KVF_PACK_AUTO}
+    for x in filter(None, a.schedules.split(",")):
+        nm, _, prm = x.partition(":")
+        configs.append((names[nm], int(prm or 0)))
     for sched, slab in configs:
         for f in w.frames:
             f.fill_(7)
@@ -68,7 +73,8 @@ def main():
         per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps))
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
-        print(json.dumps({"schedule": "two_pass" if sched == 1 else "single_read",
+        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "stream"}[sched]
+        print(json.dumps({"schedule": sname,
                           "cluster": slab, "ms_median": round(med, 4),
                           "ms_min": round(per[0], 4), "achieved_gbs": round(ach, 1),
                           "frac": round(ach / 6558.7, 4), "bit_exact": ok,
