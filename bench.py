@@ -452,7 +452,7 @@ def ctypes_copy(dst, src):
     ctypes.memmove(ctypes.addressof(dst), ctypes.addressof(src), ctypes.sizeof(src))
 
 
-def ncu_traffic(kernel: str, config_key: str):
+def ncu_traffic(kernel: str, config_key: str, launches_per_step: int = 1):
     """DRAM bytes per launch of `kernel` from a committed ncu --set full capture
     of THIS configuration (profiles/<round>/ncu_traffic.json, written by
     tools/ncu_summary.py with the bench config key), or None: a profile of
@@ -466,8 +466,12 @@ def ncu_traffic(kernel: str, config_key: str):
         except (OSError, ValueError):
             continue
         if rec and rec.get("config") == config_key:
+            n = rec.get("launches_captured", 1)
             return {"bytes_per_launch": rec["dram_bytes_per_launch"],
-                    "source": os.path.relpath(path, ROOT) + " (" + rec["report"] + ")"}
+                    "bytes_per_step": rec.get("dram_bytes_captured", rec["dram_bytes_per_launch"])
+                    if n == launches_per_step else None,
+                    "source": os.path.relpath(path, ROOT) + " (" + rec["report"] + (
+                        f", {n} launches = one step" if n > 1 else "") + ")"}
     return None
 
 
@@ -697,11 +701,13 @@ def main():
 
     if rank == 0:
         clocks = clk.summary()
-        # one restore launch per step covers all 88 units: per-launch traffic
-        # compares with algorithmic_bytes_per_step (multi-GPU: per rank)
+        # the restore launches of one step cover all units: the ncu traffic of
+        # a capture of exactly those launches compares with
+        # algorithmic_bytes_per_step (multi-GPU: per rank)
         rkernel = "restore_band_kernel" if LAYOUTS[args.layout](w.H, w.D)[3] < 8 \
             else "restore_fast_kernel"
-        traffic = ncu_traffic(rkernel, config_key(args, world))
+        traffic = ncu_traffic(rkernel, config_key(args, world),
+                              sum(launches.values()) if launches else 1)
         line = {
             "metric": "KV restore GB/s (frames->bf16 paged KV), 32K ctx",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -710,7 +716,7 @@ def main():
             "data": "synthetic", "config": workload_config(args, world, l2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic and traffic["bytes_per_launch"],
+                         "traffic": traffic and traffic["bytes_per_step"],
                          "traffic_source": traffic["source"] if traffic else
                          "no ncu capture of this configuration committed",
                          "peak_kind": peak_kind,

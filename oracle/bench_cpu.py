@@ -95,6 +95,9 @@ def run(kind="restore", workers=None, units_per_worker=2, T=10000, H=8, D=128, r
     """
     workers = workers or os.cpu_count() or 1
     fn = {"restore": restore_worker, "pack": pack_worker, "decode": decode_worker}[kind]
+    if kind == "decode":
+        from oracle import ref
+        ref.build_c()  # once, before the workers load it
     jobs = [(w + 1, units_per_worker, T, H, D, res, tuple(lay), gs) for w in range(workers)]
     if workers == 1:
         res_list = [fn(jobs[0])]

@@ -186,8 +186,11 @@ def build_c(force=False):
     src = os.path.join(HERE, "kvfc_oracle.c")
     if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
         os.makedirs(out_dir, exist_ok=True)
-        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-o", so + ".tmp", src], check=True)
-        os.replace(so + ".tmp", so)
+        # per-process temporary name: concurrent builders (a process pool's
+        # workers on a fresh checkout) each rename a complete file into place
+        tmp = f"{so}.tmp{os.getpid()}"
+        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-o", tmp, src], check=True)
+        os.replace(tmp, so)
     return so
 
 

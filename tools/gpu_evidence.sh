@@ -1,0 +1,40 @@
+#!/bin/bash
+# Round evidence on one B200: default bench line, other configs / layouts, pack
+# schedule sweep, ncu launch list and --set full captures of the hot kernels.
+# Outputs under gpurun_out/ev/ (copied into profiles/<round>/ by hand).
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+O=gpurun_out/ev; mkdir -p $O
+python -m paper_2602_09725_b200.build > $O/build.txt 2>&1 || { tail -30 $O/build.txt; exit 1; }
+nvidia-smi -q > $O/nvidia_smi_q.txt 2>&1
+lscpu > $O/lscpu.txt 2>&1
+if [ -z "$SKIP_BENCH" ]; then
+timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench rc=$?"
+for cfg in "--layout paper" "--layout col1" "--layout a2b4" "--res R240" \
+           "--model qwen2.5-7b --tokens 131072" "--model llama3-70b --tokens 81920"; do
+  tag=$(echo "$cfg" | tr -d '-' | tr ' ' '_')
+  timeout 600 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu --no-fetch $cfg \
+     > $O/bench_$tag.json 2> $O/bench_$tag.err; echo "$tag rc=$?"
+done
+timeout 300 python tools/pack_sweep.py --clusters 0 --schedules stream,stream:16 --steps 20 > $O/pack_sweep.jsonl 2>&1
+timeout 300 python tools/pack_sweep.py --clusters 0 --schedules stream --steps 20 --layout col1 > $O/pack_sweep_col1.jsonl 2>&1
+fi
+if [ -z "$SKIP_NCU" ]; then
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $O/launches.csv python bench.py --steps 10 --warmup 3 --no-cpu > $O/ncu_launch_stdout.txt 2>&1
+echo "launch list rc=$?"
+FULL="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-fetch"
+for k in restore_fast absmax_fast pack_fast; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
+      -o $O/prof_$k -f $FULL > $O/ncu_${k}.txt 2>&1; echo "$k rc=$?"
+done
+for k in restore_band pack_band; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
+      -o $O/prof_${k}_col1 -f $FULL --layout col1 > $O/ncu_${k}.txt 2>&1; echo "$k rc=$?"
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pack_stream -s 0 -c 1 \
+    -o $O/prof_pack_stream -f python tools/pack_sweep.py --schedules stream --steps 2 > $O/ncu_pack_stream.txt 2>&1; echo "pack_stream rc=$?"
+FETCH="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_decode -s 2 -c 1 \
+    -o $O/prof_rc_decode -f $FETCH > $O/ncu_rc_decode.txt 2>&1; echo "rc_decode rc=$?"
+fi
+ls $O

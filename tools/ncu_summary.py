@@ -70,12 +70,26 @@ def report(path, out, config=None):
                 return v * {"Gbyte": 1, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9}.get(u, 1)
             traffic = gb('dram__bytes_read.sum') + gb('dram__bytes_write.sum')
             fh.write(f"\nDRAM traffic per launch: {traffic:.3f} GB\n")
+            # a capture of every launch of one step (-c N): the step's traffic
+            step_traffic, n_launch = 0.0, 0
+            for r in rows[2:]:
+                if len(r) == len(h) and r[h.index("Kernel Name")] == vals[h.index("Kernel Name")]:
+                    def gbr(k, r=r):
+                        v = float(r[h.index(k)].replace(",", ""))
+                        u = units[h.index(k)]
+                        return v * {"Gbyte": 1, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9}.get(u, 1)
+                    step_traffic += gbr('dram__bytes_read.sum') + gbr('dram__bytes_write.sum')
+                    n_launch += 1
+            if n_launch > 1:
+                fh.write(f"DRAM traffic of the {n_launch} captured launches (one step): "
+                         f"{step_traffic:.3f} GB\n")
             # machine-readable: bench.py reports it as roofline.traffic
             tj = os.path.join(os.path.dirname(out), "ncu_traffic.json")
             data = json.load(open(tj)) if os.path.exists(tj) else {}
             short = name.split("(")[0].split("::")[-1].split("<")[0]
             data[short] = {"dram_bytes_per_launch": traffic * 1e9, "report": os.path.basename(path),
-                           "config": config,
+                           "config": config, "launches_captured": n_launch,
+                           "dram_bytes_captured": step_traffic * 1e9,
                            "duration": vals[h.index("gpu__time_duration.sum")] + " "
                            + units[h.index("gpu__time_duration.sum")]}
             json.dump(data, open(tj, "w"), indent=1, sort_keys=True)
