@@ -252,6 +252,9 @@ class Workload:
         self._lib, self._dev, self._L = _lib, _dev, L
         self.n_launch_restore = (len(self.units) + _lib.KVF_MAX_UNITS - 1) // _lib.KVF_MAX_UNITS
         self.n_launch_pack = 4 * self.n_launch_restore
+        # the sources, zeroed scratch and block table were produced on the
+        # current stream; callers pack/restore on streams of their own
+        torch.cuda.synchronize()
 
     def check_restored(self, per_unit=16):
         """Sampled slots of the restored caches against an independent path:
