@@ -279,6 +279,34 @@ typedef struct kvf_rc_stream {
 kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_streams,
                          void* stream);
 
+/* One contiguous byte range of a fed decode: host -> device. */
+typedef struct kvf_feed_seg {
+  const uint8_t* src;      /* pinned host memory (device-accessible through UVA) */
+  uint8_t* dst;            /* device */
+  int64_t len;
+} kvf_feed_seg;
+
+/* kvf_rc_decode whose payload bytes are still on the host: ONE cooperative
+ * launch in which n_copy_ctas CTAs copy the segments host -> device over PCIe
+ * in piece-major order (piece r of a segment = its bytes in [L0 + r*piece_bytes,
+ * L0 + (r+1)*piece_bytes), L0 = the 128-byte line holding its first byte;
+ * piece r of every segment before piece r+1 of any) while the other CTAs
+ * decode; stream k
+ * (whose payload lies in segment d_seg_of[k]) reads a byte only once the
+ * pieces of its segment up to that byte have landed.  Every stream thus starts
+ * decoding after its segment's first piece, not after the whole batch's H2D.
+ * `ready`: device scratch of n_segs u32 (zeroed here).  max_seg_len >= every
+ * segment's len.  KVF_EUNSUPPORTED if the grid does not fit one wave.  The
+ * segments (d_segs, d_seg_of: device-accessible) must cover every payload byte,
+ * each in 128-byte lines of its own (no line shared with another segment: the
+ * decoders read through L1), src and dst alike modulo 16; piece_bytes a
+ * multiple of 128.  When the call's work completes, all segments are on the
+ * device. */
+kvf_status kvf_rc_decode_fed(const kvf_rc_stream* d_streams, int32_t n_streams,
+                             const kvf_feed_seg* d_segs, const int32_t* d_seg_of,
+                             int32_t n_segs, int32_t piece_bytes, int64_t max_seg_len,
+                             uint32_t* ready, int32_t n_copy_ctas, void* stream);
+
 /* One plane of one frame for reconstruction (fk/codec.py:131-144). */
 typedef struct kvf_recon_plane {
   const uint8_t* symbols;  /* device, height*width zigzag symbols */

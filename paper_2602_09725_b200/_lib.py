@@ -92,6 +92,14 @@ class kvf_rc_stream(C.Structure):
     ]
 
 
+class kvf_feed_seg(C.Structure):
+    _fields_ = [
+        ("src", C.c_void_p),
+        ("dst", C.c_void_p),
+        ("len", C.c_int64),
+    ]
+
+
 class kvf_recon_plane(C.Structure):
     _fields_ = [
         ("symbols", C.c_void_p),
@@ -158,6 +166,8 @@ _SIGNATURES = {
     "kvf_kvfc_scan": (C.c_int, [_VP, C.c_int64, C.POINTER(kvf_kvfc_info), _VP, _VP, _VP, _VP,
                                 C.c_int32, C.POINTER(C.c_int32)]),
     "kvf_rc_decode": (C.c_int, [_VP, C.c_int32, _VP]),
+    "kvf_rc_decode_fed": (C.c_int, [_VP, C.c_int32, _VP, _VP, C.c_int32, C.c_int32, C.c_int64,
+                                    _VP, C.c_int32, _VP]),
     "kvf_kvfc_reconstruct": (C.c_int, [_VP, _VP, C.c_int32, _VP]),
     "kvf_kvfc_residuals": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP]),
     "kvf_rc_encode": (C.c_int, [_VP, C.c_int32, _VP, _VP]),

@@ -34,6 +34,7 @@ _PLANE_DTYPE = np.dtype([("symbols", "<u8"), ("modes", "<u8"), ("out", "<u8"),
                          ("out_pitch", "<i8")])
 _CHAIN_DTYPE = np.dtype([("first", "<i4"), ("count", "<i4"), ("height", "<i4"),
                          ("width", "<i4")])
+_SEG_DTYPE = np.dtype([("src", "<u8"), ("dst", "<u8"), ("len", "<i8")])
 _RESID_DTYPE = np.dtype([("cur", "<u8"), ("prev", "<u8"), ("pitch", "<i8"), ("symbols", "<u8"),
                          ("modes", "<u8"), ("height", "<i4"), ("width", "<i4")])
 _PIECE_DTYPE = np.dtype([("src", "<u8"), ("dst_off", "<i8"), ("len", "<i8"), ("pack_bits", "<i4"),
@@ -216,6 +217,10 @@ def _decode_batch(streams, out, stream, ranges, indices, max_parts, staged):
     pinned_in = all(isinstance(x, torch.Tensor) for x in streams) and len(streams) > 0
     datas = list(streams) if pinned_in else [_as_bytes(x) for x in streams]
     s = stream if stream is not None else torch.cuda.current_stream()
+    if pinned_in and indices is None and ranges is None and _fed_eligible(datas):
+        fed = _decode_fed(datas, out, s, dev)
+        if fed is not None:
+            return fed
     # Whole pinned streams with nothing to scan first: their bytes go to the
     # copy engine at once and the host walk (kvf_kvfc_scan) runs meanwhile.
     early = pinned_in and indices is None and ranges is None
@@ -326,6 +331,104 @@ def _decode_batch(streams, out, stream, ranges, indices, max_parts, staged):
     return frames, held
 
 
+# Fed decode (kvf_rc_decode_fed): long planes (R640/R1080-sized, >= this many
+# symbols) decode for ~0.33 us a symbol on one thread's serial chain, longer
+# than the whole H2D of a batch.  Their bytes are copied by the decode launch
+# itself, piece-major, so every plane starts after its first piece instead of
+# after the batch's last copy.
+_FED_MIN_SYMBOLS = 98_304
+_FED_PIECE = 16 * 1024
+_FED_COPY_CTAS = 128
+
+
+def _fed_eligible(datas):
+    """Whole pinned KVFC streams whose planes are long (header only: u32
+    n_frames, height, width, fk/codec.py:16-20)."""
+    for d in datas:
+        if d.numel() < 12 or not d.is_pinned():
+            return False
+        n, h, w = np.frombuffer(d.numpy()[:12].tobytes(), "<u4")
+        if n == 0 or int(h) * int(w) < _FED_MIN_SYMBOLS:
+            return False
+    return True
+
+
+def _decode_fed(datas, out, s, dev):
+    """decode_batch of whole pinned streams through one kvf_rc_decode_fed
+    launch + one reconstruction launch on `s`; None if the batch does not fit
+    one wave (the caller then takes the part pipeline)."""
+    idxs = index_streams(datas)
+    ranges = [(0, ix.n) for ix in idxs]
+    # Copy segments: plane k of stream j = its bytes from the previous
+    # payload's end (0 for the first) to the end of its payload (bitmap, length,
+    # payload).  Each segment gets 128-byte lines of its own in the blob, at the
+    # source's offset modulo 128 (16-byte copies; no L1 line shared with bytes
+    # that land later).
+    lo_l, len_l, src_l = [], [], []
+    for j, ix in enumerate(idxs):
+        ends = (ix.payload_off + ix.payload_len).astype(np.int64)
+        lo = np.concatenate([[0], ends[:-1]]).astype(np.int64)
+        lo_l.append(lo)
+        len_l.append(ends - lo)
+        src_l.append(datas[j].data_ptr() + lo)
+    lo_a = np.concatenate(lo_l) if lo_l else np.zeros(0, np.int64)
+    len_a = np.concatenate(len_l) if len_l else np.zeros(0, np.int64)
+    src_a = np.concatenate(src_l) if src_l else np.zeros(0, np.int64)
+    region = (len_a + 255) // 128 * 128                  # >= len + (src % 128), lines
+    roff = np.concatenate([[0], np.cumsum(region)])
+    blob = _scratch(s, "blob", int(roff[-1]) or 1)
+    base = blob.data_ptr()
+    if base % 128:
+        return None
+    dst_a = base + roff[:-1] + src_a % 128
+    hw_all = np.array([ix.h * ix.w for ix in idxs], np.int64)
+    hw16_all = -(-hw_all // 16) * 16
+    nf_all = np.array([f1 - f0 for f0, f1 in ranges], np.int64)
+    sym_at = np.concatenate([[0], np.cumsum(3 * nf_all * hw16_all)])
+    symbols = _scratch(s, "symbols", max(int(sym_at[-1]), 1))
+    if callable(out):
+        with torch.cuda.stream(s):
+            out = out([(f1 - f0, 3, ix.h, ix.w) for ix, (f0, f1) in zip(idxs, ranges)])
+    frames = []
+    with torch.cuda.stream(s):
+        for j, (ix, (f0, f1)) in enumerate(zip(idxs, ranges)):
+            fr = out[j] if out is not None else torch.empty((f1 - f0, 3, ix.h, ix.w),
+                                                           dtype=torch.uint8, device=dev)
+            if tuple(fr.shape) != (f1 - f0, 3, ix.h, ix.w):
+                raise ValueError("output frames have the wrong shape")
+            frames.append(fr)
+    part = list(range(len(datas)))
+    spans = [(0, int(d.numel())) for d in datas]
+    starts = np.zeros(len(datas) + 1, np.int64)
+    rc, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, 0,
+                                         symbols.data_ptr() + sym_at, frames,
+                                         seg_map=(lo_a, dst_a))
+    segs = np.empty(len(len_a), _SEG_DTYPE)
+    segs["src"], segs["dst"], segs["len"] = src_a, dst_a, len_a
+    if len(segs) != len(rc):
+        return None
+    seg_of = np.arange(len(rc), dtype=np.int32)
+    h_rc, h_planes, h_chains = (_pinned_copy(x) for x in (rc, flat, ch_arr))
+    h_segs, h_of = _pinned_copy(segs), _pinned_copy(seg_of)
+    ready = _scratch(s, "fed_ready", 4 * max(len(rc), 1))
+    sp = _dev.stream_ptr(s)
+    st = _lib.load().kvf_rc_decode_fed(
+        C.c_void_p(h_rc.data_ptr()), len(rc), C.c_void_p(h_segs.data_ptr()),
+        C.c_void_p(h_of.data_ptr()), len(segs), _FED_PIECE, int(segs["len"].max(initial=0)),
+        C.c_void_p(ready.data_ptr()), _FED_COPY_CTAS, sp)
+    if st == _lib.KVF_EUNSUPPORTED:
+        return None
+    _lib.check(st)
+    if len(ch_arr):
+        _lib.call("kvf_kvfc_reconstruct", C.c_void_p(h_planes.data_ptr()),
+                  C.c_void_p(h_chains.data_ptr()), len(ch_arr), sp)
+    _hold_until(s, [h_rc, h_planes, h_chains, h_segs, h_of])
+    held = blob.numel() + symbols.numel() + sum(f.numel() for f in frames)
+    for t in (blob, symbols, ready, *frames):
+        t.record_stream(s)
+    return frames, held
+
+
 def _enqueue_copies(s, parts, datas, spans, starts, blob, host):
     """Queue each part's H2D copies on its side stream (after the work `s` has
     so far); returns the side streams (just [s] for a single part)."""
@@ -399,11 +502,13 @@ def _hold_until(stream, tensors):
         _HELD.append((ev, tensors))
 
 
-def _part_descriptors(part, idxs, ranges, starts, spans, base, sym_ptr, frames):
+def _part_descriptors(part, idxs, ranges, starts, spans, base, sym_ptr, frames, seg_map=None):
     """kvf_rc_stream / kvf_recon_plane / kvf_recon_chain arrays of the streams
     `part` (indices into idxs), vectorised over their planes.  Plane k = 3 f +
     p of stream j (frame-major), streams in order; `starts` are blob offsets
-    of the copied spans, `sym_ptr[j]` the device symbol slots of stream j."""
+    of the copied spans, `sym_ptr[j]` the device symbol slots of stream j.
+    `seg_map` = (lo, dst) per plane (fed decode): the plane's bytes from stream
+    offset lo on sit at device address dst."""
     nl = len(part)
     nf = np.array([ranges[j][1] - ranges[j][0] for j in part], np.int64)
     hs = np.array([idxs[j].h for j in part], np.int64)
@@ -426,14 +531,21 @@ def _part_descriptors(part, idxs, ranges, starts, spans, base, sym_ptr, frames):
     out_ptr = np.array([frames[j].data_ptr() for j in part], np.int64)
     st = np.array([frames[j].stride()[:3] for j in part], np.int64).reshape(nl, 3)
     rc = np.empty(K, _RC_DTYPE)
-    rc["payload"] = sbase[sid] + p_off
+    if seg_map is not None:
+        lo, dst = seg_map
+        rc["payload"] = dst + (p_off - lo)
+    else:
+        rc["payload"] = sbase[sid] + p_off
     rc["len"] = p_len
     rc["symbols"] = np.asarray(sym_ptr)[part][sid] + loc * hw16[sid]
     rc["n_symbols"] = hw[sid]
     fl, pp = loc // 3, loc % 3
     pl = np.empty(K, _PLANE_DTYPE)
     pl["symbols"] = rc["symbols"]
-    pl["modes"] = np.where(b_off >= 0, sbase[sid] + b_off, 0)
+    if seg_map is not None:
+        pl["modes"] = np.where(b_off >= 0, dst + (b_off - lo), 0)
+    else:
+        pl["modes"] = np.where(b_off >= 0, sbase[sid] + b_off, 0)
     pl["out"] = out_ptr[sid] + fl * st[sid, 0] + pp * st[sid, 1]
     pl["out_pitch"] = st[sid, 2]
     ftype = np.concatenate([idxs[j].frame_type[ranges[j][0]:ranges[j][1]] for j in part])

@@ -32,13 +32,44 @@ using namespace rc;
 // shifts in the word prefetched one refill earlier (`nxt`), so the load never
 // sits on the decode chain.  Loads use clamped in-bounds addresses and bytes
 // at or past the end read as 0 (fk/rangecoder.py:158,181: data[pos] if pos < n).
+// FED: the payload is still being copied in (kvf_rc_decode_fed): a word is
+// read only once the pieces holding it landed (`ready` pieces of the stream's
+// copy segment, acquire).  Pieces end on 128-byte lines, so a line a thread
+// caches in L1 never holds bytes that land later.
+template <bool FED>
 struct ByteWindow {
   uint64_t win;
   uintptr_t wa, a, end, last;  // last = the last aligned word holding payload bytes
   uint32_t nxt;                // raw word at wa + 8 (loaded one refill ahead)
   bool nxt_ok;                 // wa + 8 < end: otherwise it reads as 0
-  __device__ __forceinline__ uint32_t load(uintptr_t w) const {  // in bounds, unmasked
-    return __ldg(reinterpret_cast<const uint32_t*>(w < end ? w : last));
+  // FED only: bytes below `avail` have landed; segment start, piece size, counter
+  uintptr_t avail, seg0;
+  uint32_t piece;
+  const uint32_t* ready;
+  __device__ __forceinline__ void await(uintptr_t need) {  // bytes below need landed
+    if (!FED) return;
+    need = need < end ? need : end;
+    if (avail < need) avail = await_slow(ready, seg0, piece, need);
+  }
+  // Polls the segment's landed-piece count until `need` is covered (out of
+  // line: the decode loop only carries the compare).
+  static __device__ __noinline__ uintptr_t await_slow(const uint32_t* ready, uintptr_t seg0,
+                                                      uint32_t piece, uintptr_t need) {
+    for (;;) {
+      uint32_t r;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(ready) : "memory");
+      const uintptr_t av = seg0 + (uintptr_t)r * piece;
+      if (av >= need) return av;
+      __nanosleep(256);
+    }
+  }
+  __device__ __forceinline__ uint32_t ld(uintptr_t w) const {
+    return __ldg(reinterpret_cast<const uint32_t*>(w));
+  }
+  __device__ __forceinline__ uint32_t load(uintptr_t w) {  // in bounds, unmasked
+    const uintptr_t x = w < end ? w : last;
+    await(x + 4);
+    return ld(x);
   }
   __device__ __forceinline__ void init(const uint8_t* p, uint32_t n) {
     a = reinterpret_cast<uintptr_t>(p);
@@ -80,6 +111,7 @@ struct ByteWindow {
     // predicated load straight into `nxt`: no instruction consumes it until
     // the next refill, so its latency never stalls the decode chain
     const uintptr_t src = wa + 8 < end ? wa + 8 : last;
+    // (FED: the block-level wait of rc_decode_kernel covers this prefetch)
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.u32 %0, [%1];\n}"
         : "+r"(nxt)
@@ -88,21 +120,105 @@ struct ByteWindow {
   }
 };
 
+#ifdef KVF_TRACE
+// trace builds (tools/trace_fed.py): globaltimer per stream [start, first
+// bytes, done] and per copy CTA [done]
+__device__ unsigned long long* g_fed_trace;
+__device__ __forceinline__ void fed_mark(int i, int e) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (g_fed_trace) g_fed_trace[(size_t)i * 4 + e] = t;
+}
+#else
+__device__ __forceinline__ void fed_mark(int, int) {}
+#endif
+
+// The copy side of kvf_rc_decode_fed: CTAs [0, n_copy) move the segments
+// host -> device over PCIe (16-byte loads of mapped pinned memory), piece r of
+// every segment before piece r+1 of any, and count each segment's landed
+// pieces in ready[] (in order, release).
+constexpr uint32_t kFedBlock = 512;  // symbols decoded per landed-bytes check
+
+struct FeedArgs {
+  const kvf_feed_seg* segs;
+  const int32_t* seg_of;  // stream -> segment
+  uint32_t* ready;
+  int32_t n_segs, n_copy, piece, rounds;
+};
+
+__device__ void copy_pieces(const FeedArgs& F) {
+  const int lane = threadIdx.x;
+  const int64_t n_t = (int64_t)F.rounds * F.n_segs;
+  for (int64_t t = blockIdx.x; t < n_t; t += F.n_copy) {
+    const int r = (int)(t / F.n_segs), k = (int)(t - (int64_t)r * F.n_segs);
+    const kvf_feed_seg sg = F.segs[k];
+    // piece r = the segment's bytes in [L0 + r P, L0 + (r+1) P), L0 = its
+    // first 128-byte line: piece ends fall on line boundaries
+    const int64_t head0 = (int64_t)(reinterpret_cast<uintptr_t>(sg.dst) & 127);
+    const int64_t lo = max((int64_t)0, (int64_t)r * F.piece - head0);
+    const int64_t hi = min(sg.len, (int64_t)(r + 1) * F.piece - head0);
+    if (lo >= hi) continue;
+    const uint8_t* src = sg.src + lo;
+    uint8_t* dst = sg.dst + lo;
+    const int64_t n = hi - lo;
+    // bytes up to 16-aligned dst, then 16-byte vectors when src is aligned alike
+    const int64_t head = min(n, (int64_t)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+    for (int64_t e = lane; e < head; e += 32) dst[e] = src[e];
+    const bool vec = ((reinterpret_cast<uintptr_t>(src + head) & 15) == 0);
+    const int64_t nv = vec ? (n - head) / 16 : 0;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+#pragma unroll 4
+    for (int64_t e = lane; e < nv; e += 32) d4[e] = ld_nc_v4(s4 + e);
+    for (int64_t e = head + nv * 16 + lane; e < n; e += 32) dst[e] = src[e];
+    __threadfence();  // this lane's bytes before the count
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t* rd = F.ready + k;
+      uint32_t cur;
+      do {  // piece r - 1 of this segment (an earlier ticket) counted first
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(rd) : "memory");
+      } while (cur != (uint32_t)r);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(rd), "r"((uint32_t)r + 1) : "memory");
+    }
+  }
+}
+
+template <bool FED>
 __global__ void __launch_bounds__(kDecThreads)
-    rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n) {
+    rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n, const FeedArgs F) {
   extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B
   __shared__ uint4 T_add[2 * kAddRows];  // increment rows (rc::add_table_init)
+  if (FED && (int)blockIdx.x < F.n_copy) {
+    copy_pieces(F);
+    if (threadIdx.x == 0) fed_mark(n + blockIdx.x, 3);
+    return;
+  }
   add_table_init(T_add);       // the whole warp, before any thread leaves
   const int tid = threadIdx.x;
-  const int sidx = blockIdx.x * kDecThreads + tid;
+  const int sidx = ((int)blockIdx.x - (FED ? F.n_copy : 0)) * kDecThreads + tid;
+  const unsigned live = __ballot_sync(0xffffffffu, sidx < n);  // the warp's streams
   if (sidx >= n) return;
   const kvf_rc_stream st = streams[sidx];
   uint4* m = M + tid;  // chunk c of this thread's model at m[c * kDecThreads]
   uint32_t P[8];       // block prefixes CB[2w] | CB[2w+1] << 16
   model_init(m, P);
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu, code = 0;
-  ByteWindow bw;
+  ByteWindow<FED> bw;
+  if (FED) {
+    const int k = F.seg_of[sidx];
+    bw.seg0 = reinterpret_cast<uintptr_t>(F.segs[k].dst) & ~uintptr_t(127);  // piece origin
+    bw.piece = (uint32_t)F.piece;
+    bw.ready = F.ready + k;
+    bw.avail = 0;
+  }
+  if (FED) fed_mark(sidx, 0);
   bw.init(st.payload, (uint32_t)st.len);
+  // FED: the warp's 32 streams start together once each has its first bytes.
+  // A thread that started alone would run its whole decode loop while the
+  // warp's waiting threads are never scheduled (divergent paths serialise).
+  if (FED) __syncwarp(live);
+  if (FED) fed_mark(sidx, 1);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     code = (code << 8) | bw.peek();
@@ -115,7 +231,16 @@ __global__ void __launch_bounds__(kDecThreads)
   uint32_t pack = 0;
   const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
   float rcp = rcp_approx(total);  // ~1/total of the symbol being decoded
-  for (uint32_t k = 0; k < nsym; ++k) {
+  // FED: blocks of kFedBlock symbols, each started only once the next
+  // kFedBlock * 8 + 16 payload bytes have landed.  A symbol takes at most 7
+  // bytes (at most 3 in the closed-form shift, then rng >= 1 needs at most 3
+  // more shifts to reach 2^24, where the top bytes of low and low + rng always
+  // differ, fk/rangecoder.py:171-183) and the window prefetch reads 12 bytes
+  // ahead, so no read inside a block passes the landed bytes.
+  for (uint32_t k0 = 0; k0 < nsym; k0 += kFedBlock) {
+  if (FED) bw.await(bw.a + kFedBlock * 8 + 16);
+  const uint32_t k1 = min(nsym, k0 + kFedBlock);
+  for (uint32_t k = k0; k < k1; ++k) {
     const float rcp_next = rcp_approx(total + kInc);  // off the chain
     const uint32_t r = exact_div(rng, total, rcp);  // rng / total (fk/rangecoder.py:163)
     // Largest s with cum(s) <= min((code - low) / r, total - 1) (fk/rangecoder.py:
@@ -221,10 +346,12 @@ __global__ void __launch_bounds__(kDecThreads)
       rcp = rcp_approx(total);
     }
   }
+  }
   if (nsym & 3) {  // tail: the last nsym % 4 symbols sit in the top bytes of `pack`
     const uint32_t base = nsym & ~3u, n_tail = nsym & 3;
     for (uint32_t k = base; k < nsym; ++k) out[k] = (uint8_t)(pack >> (8 * (4 - n_tail + k - base)));
   }
+  if (FED) fed_mark(sidx, 2);
 }
 
 // ----------------------------------------------------------- reconstruction
@@ -461,9 +588,62 @@ extern "C" kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_st
   // CTAs (448 streams) are resident per SM and the grid spreads over every SM.
   const size_t smem = (size_t)kDecThreads * 256 * sizeof(uint16_t);
   const int grid = (n_streams + kDecThreads - 1) / kDecThreads;
-  rc_decode_kernel<<<grid, kDecThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(d_streams,
-                                                                                      n_streams);
+  FeedArgs none{};
+  rc_decode_kernel<false><<<grid, kDecThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      d_streams, n_streams, none);
   KVF_CHECK_CUDA(cudaGetLastError());
+  return KVF_OK;
+}
+
+extern "C" kvf_status kvf_rc_decode_fed(const kvf_rc_stream* d_streams, int32_t n_streams,
+                                        const kvf_feed_seg* d_segs, const int32_t* d_seg_of,
+                                        int32_t n_segs, int32_t piece_bytes, int64_t max_seg_len,
+                                        uint32_t* ready, int32_t n_copy_ctas, void* stream) {
+  if (n_streams < 0 || n_segs < 0 || (n_streams > 0 && (!d_streams || !d_seg_of)) ||
+      (n_segs > 0 && (!d_segs || !ready)))
+    KVF_FAIL(KVF_EINVAL, "bad stream / segment arrays");
+  if (piece_bytes < 256 || piece_bytes % 128 || n_copy_ctas < 1 || max_seg_len < 0)
+    KVF_FAIL(KVF_EINVAL, "bad piece size / copy CTA count");
+  if (n_streams == 0 && n_segs == 0) return KVF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n_segs) KVF_CHECK_CUDA(cudaMemsetAsync(ready, 0, sizeof(uint32_t) * n_segs, s));
+  const int grid = n_copy_ctas + (n_streams + kDecThreads - 1) / kDecThreads;
+  // every CTA co-resident (decoders wait on copiers): a cooperative launch.
+  // The shared memory request spreads the CTAs over the SMs (a cooperative
+  // grid is packed; serial decode chains sharing a scheduler slow each other)
+  int dev = 0, sms = 0, per_sm = 0, smem_sm = 0;
+  KVF_CHECK_CUDA(cudaGetDevice(&dev));
+  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  const int want_per_sm = std::max(1, (grid + sms - 1) / sms);
+  size_t smem = (size_t)kDecThreads * 256 * sizeof(uint16_t);
+  smem = std::max(smem, (size_t)(smem_sm / want_per_sm) - 2048);
+  smem = std::min<size_t>(smem, 200 * 1024);
+  KVF_CHECK_CUDA(cudaFuncSetAttribute(rc_decode_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  KVF_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rc_decode_kernel<true>,
+                                                               kDecThreads, smem));
+  if ((int64_t)per_sm * sms < grid)
+    KVF_FAIL(KVF_EUNSUPPORTED, "fed decode of %d streams does not fit one wave", n_streams);
+  FeedArgs F;
+  F.segs = d_segs;
+  F.seg_of = d_seg_of;
+  F.ready = ready;
+  F.n_segs = n_segs;
+  F.n_copy = n_copy_ctas;
+  F.piece = piece_bytes;
+  F.rounds = (int32_t)((max_seg_len + 127 + piece_bytes - 1) / piece_bytes);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kDecThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KVF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, rc_decode_kernel<true>, d_streams, (int)n_streams, F));
   return KVF_OK;
 }
 
@@ -478,3 +658,9 @@ extern "C" kvf_status kvf_kvfc_reconstruct(const kvf_recon_plane* d_planes,
   KVF_CHECK_CUDA(cudaGetLastError());
   return KVF_OK;
 }
+
+#ifdef KVF_TRACE
+extern "C" int kvf_fed_trace_set(void* p) {
+  return (int)cudaMemcpyToSymbol(kvf::g_fed_trace, &p, sizeof(p));
+}
+#endif
