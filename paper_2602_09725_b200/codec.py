@@ -341,16 +341,22 @@ _FED_PIECE = 16 * 1024
 _FED_COPY_CTAS = 128
 
 
+_FED_MAX_PLANES = 50_000  # one wave of 1-warp decoder CTAs (+ copy CTAs) on 148 SMs
+
+
 def _fed_eligible(datas):
     """Whole pinned KVFC streams whose planes are long (header only: u32
-    n_frames, height, width, fk/codec.py:16-20)."""
+    n_frames, height, width, fk/codec.py:16-20), few enough planes for one
+    wave of the fed launch."""
+    planes = 0
     for d in datas:
         if d.numel() < 12 or not d.is_pinned():
             return False
         n, h, w = np.frombuffer(d.numpy()[:12].tobytes(), "<u4")
         if n == 0 or int(h) * int(w) < _FED_MIN_SYMBOLS:
             return False
-    return True
+        planes += 3 * int(n)
+    return planes <= _FED_MAX_PLANES
 
 
 def _decode_fed(datas, out, s, dev):

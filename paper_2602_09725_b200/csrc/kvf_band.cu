@@ -35,7 +35,9 @@ namespace {
 
 constexpr int kBThreads = 256;
 constexpr int kBWarps = kBThreads / 32;
-constexpr int kBandSmem = 48 * 1024;  // per CTA (default dynamic limit)
+// per CTA: the default 48 KB limit covers static + dynamic shared memory, so
+// the bands stay below it with room for the kernels' static arrays
+constexpr int kBandSmem = 46 * 1024;
 
 // Band geometry of a unit (host-derived).
 struct BandGeom {

@@ -615,3 +615,23 @@ def test_every_tiling_pack_and_restore_match_oracle(res):
                 np.testing.assert_array_equal(got.numpy(), v.reshape(T, 3, H * D), err_msg=str(lay))
             else:
                 assert torch.equal(got, torch.from_numpy(deq).to(torch.bfloat16)), lay
+
+
+def test_all_tilings_32x128_pack_and_restore():
+    """Every tiling of a 32-head x 128 cache (the reference's acceptance case,
+    tests/test_acceptance.py:112-145): assemble_frames of int8 codes and the
+    quantising pack against the oracle's frames, and the restore of those frames
+    against the oracle's codes; the narrow-row tilings take the band kernels
+    with 4096-channel slots."""
+    H, D, T = 32, 128, 8
+    x = cases.to_bf16_values(ref.gen_synthetic_kv(T, 3, H, D, 0.9, 0, 0.3))
+    v, s = ref.quantize(x, 128)
+    t = torch.from_numpy(v.reshape(T, 3, H * D)).cuda()
+    for cfg in L.tiling_candidates(H, D):
+        plan = L.plan_inter_frame(T, "R240", cfg, 4)
+        want = ref.assemble_frames(v.reshape(T, 3, H * D),
+                                   ref.Plan(T, "R240", H, D, cfg.a_h, cfg.b_h, cfg.a_d, cfg.b_d, F=4))
+        fr = L.assemble_frames(t, plan)
+        assert np.array_equal(fr.cpu().numpy(), want), cfg
+        back = L.disassemble_frames(fr, plan)
+        assert np.array_equal(back.cpu().numpy(), v.reshape(T, 3, H * D)), cfg
