@@ -198,10 +198,14 @@ typedef enum kvf_pack_schedule {
   KVF_PACK_SINGLE_READ = 2, /* thread-block clusters, one per (unit, plane, group) at a
                                time, exchange the all-token maxima through distributed
                                shared memory; the quantising re-read is an L2 hit */
-  KVF_PACK_STREAM = 3       /* one HBM read: clusters of 16 (or 8) CTAs own whole
+  KVF_PACK_STREAM = 3,      /* one HBM read: clusters of 16 (or 8) CTAs own whole
                                (unit, plane, group) sub-units, stream them through
                                shared memory with TMA, exchange the maxima through
                                distributed shared memory and re-read from L2 */
+  KVF_PACK_SPLIT = 4        /* one HBM read: a cooperative grid whose fold CTAs take the
+                               maxima of each (unit, plane) while its quantise CTAs pack
+                               the plane before, re-read from L2; `param` = per-mille of
+                               fold CTAs (0: 400) */
 } kvf_pack_schedule;
 
 /* kvf_pack_batch with an explicit schedule.  `param` (single read only): bits
@@ -222,7 +226,7 @@ kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
 kvf_status kvf_pack_frames_batch(const kvf_pack_unit* units, int32_t n_units,
                                  void* stream);
 
-/* u32 words of pack scratch a unit of this plan needs: 6*G (G = H*D/group_size). */
+/* u32 words of pack scratch a unit of this plan needs: 6*G + 8 (G = H*D/group_size). */
 int64_t kvf_pack_scratch_words(const kvf_plan* plan);
 
 /* ---- whole-tensor quantize / dequantize (fk/kvmodel.py:127-152) -------- */

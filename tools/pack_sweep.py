@@ -48,7 +48,8 @@ def main():
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
     for x in filter(None, a.clusters.split(",")):   # CTAs per cluster, 0 = auto
         configs.append((_lib.KVF_PACK_SINGLE_READ, int(x)))
-    names = {"stream": _lib.KVF_PACK_STREAM, "auto": _lib.KVF_PACK_AUTO}
+    names = {"stream": _lib.KVF_PACK_STREAM, "auto": _lib.KVF_PACK_AUTO,
+             "split": _lib.KVF_PACK_SPLIT}
     for x in filter(None, a.schedules.split(",")):
         nm, _, prm = x.partition(":")
         configs.append((names[nm], int(prm or 0)))
@@ -73,7 +74,7 @@ def main():
         per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps))
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
-        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "stream"}[sched]
+        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "stream", 4: "split"}[sched]
         print(json.dumps({"schedule": sname,
                           "cluster": slab, "ms_median": round(med, 4),
                           "ms_min": round(per[0], 4), "achieved_gbs": round(ach, 1),
