@@ -195,26 +195,18 @@ kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
 typedef enum kvf_pack_schedule {
   KVF_PACK_AUTO = 0,        /* the fastest measured on this build */
   KVF_PACK_TWO_PASS = 1,    /* absmax kernel, then frames kernel: reads the source twice */
-  KVF_PACK_SINGLE_READ = 2, /* thread-block clusters, one per (unit, plane, group) at a
-                               time, exchange the all-token maxima through distributed
-                               shared memory; the quantising re-read is an L2 hit */
-  KVF_PACK_STREAM = 3,      /* one HBM read: clusters of 16 (or 8) CTAs own whole
-                               (unit, plane, group) sub-units, stream them through
-                               shared memory with TMA, exchange the maxima through
-                               distributed shared memory and re-read from L2 */
-  KVF_PACK_SPLIT = 4        /* one HBM read: a cooperative grid whose fold CTAs take the
-                               maxima of each (unit, plane) while its quantise CTAs pack
-                               the plane before, re-read from L2; `param` = per-mille of
-                               fold CTAs (0: 400) */
+  KVF_PACK_SINGLE_READ = 2  /* one HBM read: clusters of 8 (or 16) CTAs own whole
+                               (unit, plane, group) sub-units, stream them through shared
+                               memory with TMA, exchange the maxima through distributed
+                               shared memory and re-read from L2.  Slower than two-pass on
+                               B200 */
 } kvf_pack_schedule;
 
-/* kvf_pack_batch with an explicit schedule.  `param` (single read only): bits
- * 0-7 = CTAs per cluster (16, 8, 4 or 2; 0 = the configuration covering the
- * most SMs while the sub-units in flight fit in ~45% of L2); bit 8 = drop that
- * L2 cap; bits 9-10 = CTA shape (0: 16 warps x 3 stages, 1: 12 x 4, 2: 8 x 6).
- * Same results for every schedule (bit-identical frames and scales); units a
- * schedule cannot take (int8 sources, unsupported group sizes or alignment)
- * run the two-pass kernels. */
+/* kvf_pack_batch with an explicit schedule.  `param` (single read only): CTAs
+ * per cluster, 8 or 16 (0 = 8).  Same results for every schedule (bit-identical
+ * frames and scales); units a schedule cannot take (int8 sources, group sizes
+ * other than 64/128/256, tile rows narrower than 8 channels, strides the tensor
+ * maps reject) run the two-pass kernels. */
 kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
                              int32_t schedule, int64_t param, void* stream);
 
@@ -226,7 +218,7 @@ kvf_status kvf_pack_batch_ex(const kvf_pack_unit* units, int32_t n_units,
 kvf_status kvf_pack_frames_batch(const kvf_pack_unit* units, int32_t n_units,
                                  void* stream);
 
-/* u32 words of pack scratch a unit of this plan needs: 6*G + 8 (G = H*D/group_size). */
+/* u32 words of pack scratch a unit of this plan needs: 6*G (G = H*D/group_size). */
 int64_t kvf_pack_scratch_words(const kvf_plan* plan);
 
 /* ---- whole-tensor quantize / dequantize (fk/kvmodel.py:127-152) -------- */

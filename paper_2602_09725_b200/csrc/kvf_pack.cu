@@ -8,7 +8,7 @@
 //   zero scratch -> absmax (max |x| per (plane, group) over all chunk tokens) ->
 //   scales -> frames (exact quantise + tile + place, pad tiles 128).
 // The reference scale spans all chunk tokens, so these kernels read the source
-// twice; the single-HBM-read schedule is kvf_pack_cluster.cu.
+// twice; the single-HBM-read schedule is kvf_pack_stream.cu.
 #include <algorithm>
 #include <cstdio>
 #include <vector>
@@ -17,13 +17,9 @@
 
 namespace kvf {
 
-kvf_status launch_pack_cluster(const std::vector<kvf_pack_unit>& units, int32_t dtype,
-                               int64_t param, cudaStream_t s, bool* launched);
 kvf_status launch_pack_stream(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                               int cluster, int probe, cudaStream_t s,
                               std::vector<kvf_pack_unit>* rest);
-kvf_status launch_pack_split(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                             int frac_a, int lag, cudaStream_t s, bool* launched);
 bool pack_band_ok(const kvf_pack_unit& u);
 kvf_status launch_pack_band(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                             cudaStream_t s);
@@ -323,32 +319,13 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int variant, i
   return KVF_OK;
 }
 
-// Single-read schedule: one cluster launch per launch-sized slice of units;
-// slices it cannot take run the phase-split kernels.
-kvf_status launch_single_read(const std::vector<kvf_pack_unit>& units, int32_t dtype,
-                              int64_t param, cudaStream_t s,
-                              std::vector<kvf_pack_unit>* rest) {
-  for (size_t at = 0; at < units.size(); at += kMaxPackUnits) {
-    const size_t n = std::min<size_t>(kMaxPackUnits, units.size() - at);
-    std::vector<kvf_pack_unit> part(units.begin() + at, units.begin() + at + n);
-    bool launched = false;
-    kvf_status st = launch_pack_cluster(part, dtype, param, s, &launched);
-    if (st != KVF_OK) return st;
-    if (!launched) rest->insert(rest->end(), part.begin(), part.end());
-  }
-  return KVF_OK;
-}
-
 kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t schedule,
                int64_t param, cudaStream_t s) {
   if (n_units < 0 || (n_units > 0 && units == nullptr)) KVF_FAIL(KVF_EINVAL, "bad unit array");
-  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_SPLIT)
+  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_SINGLE_READ)
     KVF_FAIL(KVF_EINVAL, "bad pack schedule %d", schedule);
   if (param < 0) KVF_FAIL(KVF_EINVAL, "negative schedule parameter");
-  const bool all = phases == (1 | 2 | 4 | 8);
-  const bool single = schedule == KVF_PACK_SINGLE_READ && all;
-  const bool stream = schedule == KVF_PACK_STREAM && all;
-  const bool split = schedule == KVF_PACK_SPLIT && all;
+  const bool single = schedule == KVF_PACK_SINGLE_READ && phases == (1 | 2 | 4 | 8);
   std::vector<kvf_pack_unit> by_dtype[4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
@@ -359,9 +336,6 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t 
   for (int dt = 0; dt < 4; ++dt) {
     std::vector<kvf_pack_unit> rest;
     if (single && dt != KVF_I8) {
-      kvf_status st = launch_single_read(by_dtype[dt], dt, param, s, &rest);
-      if (st != KVF_OK) return st;
-    } else if (stream && dt != KVF_I8) {
       kvf_status st = launch_pack_stream(by_dtype[dt], dt, (int)(param & 0xFF),
                                          (int)((param >> 8) & 0xFF), s, &rest);
       if (st != KVF_OK) return st;
@@ -377,13 +351,6 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t 
   for (int v = 0; v < kBandBase + 17; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        if (split && v >= 1 && v <= 16 && dt != KVF_I8) {
-          bool launched = false;
-          kvf_status st = launch_pack_split(groups[v][dt], v, dt, (int)(param & 0x3FF),
-                                            (int)((param >> 10) & 0xF), s, &launched);
-          if (st != KVF_OK) return st;
-          if (launched) continue;
-        }
         kvf_status st = launch_phases(groups[v][dt], v, dt, phases, s);
         if (st != KVF_OK) return st;
       }

@@ -16,10 +16,10 @@ constexpr int kPackWarps = kPackThreads / 32;
 constexpr int kMaxPackUnits = 96;  // descriptors per launch (kernel params <= 32 KB)
 
 // Scratch words of a unit (kvf_pack_scratch_words): [3, G] |x| maxima (f32
-// bit patterns) | [3, G] counter words | 8 plane counters (split schedule).
+// bit patterns) | [3, G] counter words.
 inline int64_t pack_scratch_words(const kvf_plan& p) {
   const int64_t G = (int64_t)p.H * p.D / p.group_size;
-  return 6 * G + 8;
+  return 6 * G;
 }
 
 struct PackUnitDev {

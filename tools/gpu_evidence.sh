@@ -15,8 +15,8 @@ for cfg in "--layout paper" "--layout col1" "--layout a2b4" "--res R240" \
   timeout 600 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu --no-fetch $cfg \
      > $O/bench_$tag.json 2> $O/bench_$tag.err; echo "$tag rc=$?"
 done
-timeout 300 python tools/pack_sweep.py --clusters 0 --schedules stream,stream:16 --steps 20 > $O/pack_sweep.jsonl 2>&1
-timeout 300 python tools/pack_sweep.py --clusters 0 --schedules stream --steps 20 --layout col1 > $O/pack_sweep_col1.jsonl 2>&1
+timeout 300 python tools/pack_sweep.py --schedules single_read,single_read:16 --steps 20 > $O/pack_sweep.jsonl 2>&1
+timeout 300 python tools/pack_sweep.py --schedules single_read --steps 20 --layout col1 > $O/pack_sweep_col1.jsonl 2>&1
 fi
 if [ -z "$SKIP_NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
@@ -32,7 +32,7 @@ for k in restore_band pack_band; do
       -o $O/prof_${k}_col1 -f $FULL --layout col1 > $O/ncu_${k}.txt 2>&1; echo "$k rc=$?"
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:pack_stream -s 0 -c 1 \
-    -o $O/prof_pack_stream -f python tools/pack_sweep.py --schedules stream --steps 2 > $O/ncu_pack_stream.txt 2>&1; echo "pack_stream rc=$?"
+    -o $O/prof_pack_stream -f python tools/pack_sweep.py --schedules single_read --steps 2 > $O/ncu_pack_stream.txt 2>&1; echo "pack_stream rc=$?"
 FETCH="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_decode -s 2 -c 1 \
     -o $O/prof_rc_decode -f $FETCH > $O/ncu_rc_decode.txt 2>&1; echo "rc_decode rc=$?"

@@ -5,7 +5,7 @@ reference result, then times each schedule and checks that its frames and
 scales are bit-identical.  One JSON line per schedule.
 
     python tools/pack_sweep.py [--model llama3-8b --tokens 32768 --layout identity]
-                               [--clusters 0,16,8] [--steps 20]
+                               [--schedules single_read,single_read:16,auto] [--steps 20]
 """
 import argparse
 import json
@@ -27,8 +27,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=32768)
     ap.add_argument("--layout", default="identity")
     ap.add_argument("--res", default="R1080")
-    ap.add_argument("--clusters", default="")
-    ap.add_argument("--schedules", default="stream", help="comma list of stream / auto")
+    ap.add_argument("--schedules", default="single_read",
+                    help="comma list of single_read[:cluster] / auto")
     ap.add_argument("--steps", type=int, default=20)
     a = ap.parse_args()
     args = argparse.Namespace(model=a.model, tokens=a.tokens, layout=a.layout, res=a.res, page=16,
@@ -46,10 +46,7 @@ def main():
     ref_frames = [f.clone() for f in w.frames]
     ref_scales = [x.clone() for x in w.scales]
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
-    for x in filter(None, a.clusters.split(",")):   # CTAs per cluster, 0 = auto
-        configs.append((_lib.KVF_PACK_SINGLE_READ, int(x)))
-    names = {"stream": _lib.KVF_PACK_STREAM, "auto": _lib.KVF_PACK_AUTO,
-             "split": _lib.KVF_PACK_SPLIT}
+    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO}
     for x in filter(None, a.schedules.split(",")):
         nm, _, prm = x.partition(":")
         configs.append((names[nm], int(prm or 0)))
@@ -74,7 +71,7 @@ def main():
         per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps))
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
-        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "stream", 4: "split"}[sched]
+        sname = {0: "auto", 1: "two_pass", 2: "single_read"}[sched]
         print(json.dumps({"schedule": sname,
                           "cluster": slab, "ms_median": round(med, 4),
                           "ms_min": round(per[0], 4), "achieved_gbs": round(ach, 1),

@@ -1,7 +1,7 @@
 """Stage trace of the stream pack schedule (kvf_pack_stream.cu built with -DKVF_TRACE).
 
 Builds a trace variant of libkvf into gpurun_out/trace/, packs C2 (bench.Workload)
-with KVF_PACK_STREAM through it and prints per-stage latency percentiles over
+with KVF_PACK_SINGLE_READ through it and prints per-stage latency percentiles over
 the steady-state items of every CTA (globaltimer ns):
   empty wait (producer), TMA + fold, fold -> published, fold -> ready (all CTAs),
   ready -> Q start, Q time, issue -> slot free.
@@ -62,7 +62,7 @@ def main():
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(s)
-        rc = tl.kvf_pack_batch_ex(arr, min(80, len(w.pack_units)), _lib.KVF_PACK_STREAM, a.param,
+        rc = tl.kvf_pack_batch_ex(arr, min(80, len(w.pack_units)), _lib.KVF_PACK_SINGLE_READ, a.param,
                                   _dev.stream_ptr(s))
         ev1.record(s)
         torch.cuda.synchronize()
