@@ -169,6 +169,20 @@ kvf_status kvf_restore(const kvf_surface* frames, int32_t first_frame,
 kvf_status kvf_restore_batch(const kvf_restore_unit* units, int32_t n_units,
                              void* stream);
 
+/* kvf_restore_batch restricted to KV heads, for tensor-parallel caches that
+ * hold a head shard: heads [head_lo, head_lo +
+ * n_windows*n_heads) in n_windows windows of n_heads; head h of window
+ * w = (h - head_lo) / n_heads lands at local head (h - head_lo) % n_heads of
+ * `dst`, displaced by w * window_stride bytes (a peer's region of a send buffer;
+ * one window: a rank's own shard).  raw_samples = 1 (int8 destinations only)
+ * stores the frame samples (q + 128) instead of the codes: the head slice in
+ * frame form, which a peer restores with kvf_restore_batch under a flat plan
+ * (identity tile of n_heads x D, F = 1, one frame of T tile rows).  Only the
+ * windows' bytes are read and written. */
+kvf_status kvf_restore_batch_heads(const kvf_restore_unit* units, int32_t n_units,
+                                   int32_t head_lo, int32_t n_heads, int32_t n_windows,
+                                   int64_t window_stride, int32_t raw_samples, void* stream);
+
 /* ---- pack (KV -> frames) ------------------------------------------------ */
 
 /* Phase 1: per (plane, group) max |x| over all chunk tokens, accumulated with

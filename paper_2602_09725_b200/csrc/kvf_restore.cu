@@ -15,6 +15,7 @@
 //
 // Bound: HBM.  Algorithmic bytes per channel element: 1 (u8 read) + sizeof(out).
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "kvf_common.cuh"
@@ -34,7 +35,13 @@ constexpr int kIPW = 4;  // item rounds per warp (loads in flight per lane: kIPW
 // SUB = 4 / VPL items side by side in a warp, 32 / SUB lanes each, so every
 // lane still moves 4 vectors per item round and the per-item index math is
 // amortised over as many bytes as for C = 1024.
-__host__ __device__ constexpr int sub_for(int vpl) { return vpl >= 4 ? 1 : 4 / vpl; }
+// VPL 0 stands for C = 128 channels (half a vector per lane of a 32-lane
+// item): 8 items side by side, 4 lanes of 4 vectors each.
+__host__ __device__ constexpr int sub_for(int vpl) {
+  return vpl == 0 ? 8 : (vpl >= 4 ? 1 : 4 / vpl);
+}
+__host__ __device__ constexpr int vl_for(int vpl) { return vpl == 0 ? 4 : vpl * sub_for(vpl); }
+constexpr int kVariantC128 = 3;  // restore_variant code of C = 128 (VPL 0)
 __host__ __device__ constexpr int ipw_for(int vpl) { return kIPW * sub_for(vpl); }
 
 struct RestoreUnitDev {
@@ -48,15 +55,27 @@ struct RestoreUnitDev {
   int32_t G;              // groups per layer
 };
 
+// Head windows of kvf_restore_batch_heads (the same for every unit of a launch;
+// else the whole slot: head_lo 0, head_hi = win_heads = H).
+struct HeadWin {
+  int32_t head_lo, head_hi;  // heads restored
+  int32_t win_heads;         // heads per window; window w lands at + w * win_stride
+  int32_t raw;               // int8 destination gets the samples (q + 128), not q
+  int64_t win_stride;        // bytes
+};
+
 struct RestoreParams {
   int32_t n_units;
+  HeadWin hw;
   RestoreUnitDev u[KVF_MAX_UNITS];
 };
 
 // grid = (item tiles, unit, plane): the plane (layer of the triplet) is uniform
 // per CTA, so each lane loads its VPL group scales once and the per-item index
 // math is a handful of multiply-high divisions by host-precomputed constants.
-template <int OUT, int VPL>
+// HW: head window (kvf_restore_batch_heads): only heads [head_lo, head_hi)
+// move, to local head h - head_lo of the destination.
+template <int OUT, int VPL, bool HW = false>
 __global__ void __launch_bounds__(kThreads)
     restore_fast_kernel(const __grid_constant__ RestoreParams P) {
   const RestoreUnitDev& U = P.u[blockIdx.y];
@@ -65,7 +84,7 @@ __global__ void __launch_bounds__(kThreads)
   const int lane = threadIdx.x & 31;
   constexpr int SUB = sub_for(VPL);         // items side by side in the warp
   constexpr int LPI = 32 / SUB;             // lanes per item
-  constexpr int VL = VPL * SUB;             // vectors per lane per item
+  constexpr int VL = vl_for(VPL);           // vectors per lane per item
   const int sub = lane / LPI, sl = lane % LPI;
   const int item0 = (blockIdx.x * kWarps + warp) * ipw_for(VPL);
   char* layer = reinterpret_cast<char*>(U.dst.layer[p]);
@@ -73,15 +92,27 @@ __global__ void __launch_bounds__(kThreads)
 
   constexpr int ES = OUT == KVF_F32 ? 4 : (OUT == KVF_I8 ? 1 : 2);
   int32_t in_off[VL];
-  int32_t out_off[VL];
+  using OffT = std::conditional_t<HW, int64_t, int32_t>;
+  OffT out_off[VL];
   float s[VL];
+  uint32_t live = ~0u;  // HW: the lane's vectors inside the head windows
 #pragma unroll
   for (int k = 0; k < VL; ++k) {
     int c = (sl + LPI * k) * 8;
     in_off[k] = (int32_t)tile_offset(U.g, c, U.fr.row_pitch);
-    out_off[k] = (int32_t)slot_channel_offset(U.g, c, U.dst.head_stride) * ES;
+    if constexpr (HW) {
+      const int h = c >> U.g.lg_D;
+      if (h < P.hw.head_lo || h >= P.hw.head_hi) live &= ~(1u << k);
+      const int r = h - P.hw.head_lo, w = r / P.hw.win_heads;
+      const int local = (r - w * P.hw.win_heads) << U.g.lg_D | (c & ((1 << U.g.lg_D) - 1));
+      out_off[k] = (int64_t)w * P.hw.win_stride +
+                   slot_channel_offset(U.g, local, U.dst.head_stride) * ES;
+    } else {
+      out_off[k] = (int32_t)slot_channel_offset(U.g, c, U.dst.head_stride) * ES;
+    }
     if constexpr (OUT != KVF_I8) s[k] = __ldg(U.scales + p * U.G + (c >> U.g.lg_gs));
   }
+  const uint32_t flip = (HW && P.hw.raw) ? 0u : 0x80808080u;
   const uint8_t* plane_base = U.fr.base + (int64_t)p * U.fr.plane_stride;
 
   uint2 v[kIPW][VL];
@@ -101,7 +132,8 @@ __global__ void __launch_bounds__(kThreads)
         const uint8_t* src = plane_base + (int64_t)f * U.fr.frame_stride +
                              (int64_t)tr * U.g.tile_h * U.fr.row_pitch + tc * U.g.tile_w;
 #pragma unroll
-        for (int k = 0; k < VL; ++k) v[it][k] = ld_nc_v2(src + in_off[k]);
+        for (int k = 0; k < VL; ++k)
+          if (!HW || ((live >> k) & 1)) v[it][k] = ld_nc_v2(src + in_off[k]);
         outp[it] = layer + paged_slot_offset_fd(U.dst, U.div_bs, i) * ES;
       }
     }
@@ -112,10 +144,11 @@ __global__ void __launch_bounds__(kThreads)
     if (outp[it] == nullptr) continue;
 #pragma unroll
     for (int k = 0; k < VL; ++k) {
+      if (HW && !((live >> k) & 1)) continue;
       char* dst = outp[it] + out_off[k];
       if constexpr (OUT == KVF_I8) {
         // int8 code = u8 sample - 128 = sample ^ 0x80 (fk/fetchsim.py:351).
-        st_v2(dst, make_uint2(v[it][k].x ^ 0x80808080u, v[it][k].y ^ 0x80808080u));
+        st_v2(dst, make_uint2(v[it][k].x ^ flip, v[it][k].y ^ flip));
       } else {
         float q[8];
         bytes8_to_float(v[it][k].x, v[it][k].y, q);
@@ -148,6 +181,12 @@ __global__ void __launch_bounds__(kThreads)
   void* layer = U.dst.layer[p];
   if (q_item >= U.n_plane_items || layer == nullptr) return;
   int c = (int)(x & (U.g.C - 1));
+  const int h = c >> U.g.lg_D;
+  const bool win = P.hw.win_heads > 0;  // kvf_restore_batch_heads
+  if (win && (h < P.hw.head_lo || h >= P.hw.head_hi)) return;
+  const int hr = win ? h - P.hw.head_lo : 0, hw = win ? hr / P.hw.win_heads : 0;
+  const int local = win ? ((hr - hw * P.hw.win_heads) << U.g.lg_D | (c & ((1 << U.g.lg_D) - 1)))
+                        : c;
   int fl = (int)q_item / U.g.tpf;
   int slot = (int)q_item - fl * U.g.tpf;
   int f = U.first_frame + fl;
@@ -163,8 +202,9 @@ __global__ void __launch_bounds__(kThreads)
   float val = 0.0f;
   if (U.dst.dtype != KVF_I8)
     val = (float)q * __ldg(U.scales + p * U.G + c / U.g.group_size);
-  int64_t o = paged_slot_offset(U.dst, i) + slot_channel_offset(U.g, c, U.dst.head_stride);
-  store_from_float(layer, o, U.dst.dtype, val, q);
+  int64_t o = paged_slot_offset(U.dst, i) + slot_channel_offset(U.g, local, U.dst.head_stride);
+  void* base = static_cast<char*>(layer) + (int64_t)hw * P.hw.win_stride;
+  store_from_float(base, o, U.dst.dtype, val, P.hw.raw ? q + 128 : q);
 }
 
 bool aligned(const void* p, int64_t a) {
@@ -175,9 +215,10 @@ bool aligned(const void* p, int64_t a) {
 int restore_variant(const kvf_restore_unit& u) {
   const kvf_plan& p = u.plan;
   int64_t C = (int64_t)p.H * p.D;
-  if (C % 256 != 0) return 0;
-  int vpl = (int)(C / 256);
-  if (vpl != 1 && vpl != 2 && vpl != 4 && vpl != 8 && vpl != 16) return 0;
+  if (C != 128 && C % 256 != 0) return 0;
+  int vpl = C == 128 ? kVariantC128 : (int)(C / 256);
+  if (vpl != 1 && vpl != 2 && vpl != kVariantC128 && vpl != 4 && vpl != 8 && vpl != 16)
+    return 0;
   if (p.b_d % 8 != 0) return 0;
   if (u.dst.dtype != KVF_I8 && p.group_size % 8 != 0) return 0;
   if (!aligned(u.frames.base, 8) || u.frames.frame_stride % 8 ||
@@ -229,20 +270,28 @@ RestoreUnitDev to_dev(const kvf_restore_unit& u) {
   return d;
 }
 
-template <int OUT>
+template <int OUT, bool HW>
 void launch_fast(int vpl, const RestoreParams& P, dim3 grid, cudaStream_t s) {
   switch (vpl) {
-    case 1: restore_fast_kernel<OUT, 1><<<grid, kThreads, 0, s>>>(P); break;
-    case 2: restore_fast_kernel<OUT, 2><<<grid, kThreads, 0, s>>>(P); break;
-    case 4: restore_fast_kernel<OUT, 4><<<grid, kThreads, 0, s>>>(P); break;
-    case 8: restore_fast_kernel<OUT, 8><<<grid, kThreads, 0, s>>>(P); break;
-    case 16: restore_fast_kernel<OUT, 16><<<grid, kThreads, 0, s>>>(P); break;
+    case 1: restore_fast_kernel<OUT, 1, HW><<<grid, kThreads, 0, s>>>(P); break;
+    case 2: restore_fast_kernel<OUT, 2, HW><<<grid, kThreads, 0, s>>>(P); break;
+    case kVariantC128: restore_fast_kernel<OUT, 0, HW><<<grid, kThreads, 0, s>>>(P); break;
+    case 4: restore_fast_kernel<OUT, 4, HW><<<grid, kThreads, 0, s>>>(P); break;
+    case 8: restore_fast_kernel<OUT, 8, HW><<<grid, kThreads, 0, s>>>(P); break;
+    case 16: restore_fast_kernel<OUT, 16, HW><<<grid, kThreads, 0, s>>>(P); break;
   }
 }
 
 // Launch one group of units that share (variant, dtype).
+struct HeadWindow {
+  int32_t lo, hi, win_heads, raw;
+  int64_t win_stride;
+  bool on;
+};
+
 kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
-                        int32_t dtype, cudaStream_t s) {
+                        int32_t dtype, cudaStream_t s,
+                        HeadWindow hw = {0, 0, 1, 0, 0, false}) {
   // equal launches (e.g. 280 units: 94 + 93 + 93, not 128 + 128 + 24, whose
   // last small launch would leave most SMs idle)
   const size_t n_launch = (units.size() + KVF_MAX_UNITS - 1) / KVF_MAX_UNITS;
@@ -251,6 +300,8 @@ kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
     size_t n = std::min<size_t>(per, units.size() - at);
     RestoreParams P;
     P.n_units = (int32_t)n;
+    P.hw = hw.on ? HeadWin{hw.lo, hw.hi, hw.win_heads, hw.raw, hw.win_stride}
+                 : HeadWin{0, 0, 0, 0, 0};
     int64_t max_work = 0;
     for (size_t k = 0; k < n; ++k) {
       P.u[k] = to_dev(units[at + k]);
@@ -258,18 +309,28 @@ kvf_status launch_group(const std::vector<kvf_restore_unit>& units, int vpl,
       max_work = std::max(max_work, w);
     }
     if (max_work == 0) continue;
-    int64_t per_cta = vpl ? (int64_t)kWarps * ipw_for(vpl) : kThreads;
+    int64_t per_cta =
+        vpl ? (int64_t)kWarps * ipw_for(vpl == kVariantC128 ? 0 : vpl) : kThreads;
     int64_t gx = (max_work + per_cta - 1) / per_cta;
     if (gx > 0x7FFFFFFF) KVF_FAIL(KVF_EUNSUPPORTED, "restore grid too large");
     dim3 grid((unsigned)gx, (unsigned)n, 3);
     if (vpl == 0) {
       restore_generic_kernel<<<grid, kThreads, 0, s>>>(P);
     } else {
-      switch (dtype) {
-        case KVF_BF16: launch_fast<KVF_BF16>(vpl, P, grid, s); break;
-        case KVF_F16: launch_fast<KVF_F16>(vpl, P, grid, s); break;
-        case KVF_F32: launch_fast<KVF_F32>(vpl, P, grid, s); break;
-        case KVF_I8: launch_fast<KVF_I8>(vpl, P, grid, s); break;
+      if (hw.on) {
+        switch (dtype) {
+          case KVF_BF16: launch_fast<KVF_BF16, true>(vpl, P, grid, s); break;
+          case KVF_F16: launch_fast<KVF_F16, true>(vpl, P, grid, s); break;
+          case KVF_F32: launch_fast<KVF_F32, true>(vpl, P, grid, s); break;
+          case KVF_I8: launch_fast<KVF_I8, true>(vpl, P, grid, s); break;
+        }
+      } else {
+        switch (dtype) {
+          case KVF_BF16: launch_fast<KVF_BF16, false>(vpl, P, grid, s); break;
+          case KVF_F16: launch_fast<KVF_F16, false>(vpl, P, grid, s); break;
+          case KVF_F32: launch_fast<KVF_F32, false>(vpl, P, grid, s); break;
+          case KVF_I8: launch_fast<KVF_I8, false>(vpl, P, grid, s); break;
+        }
       }
     }
     KVF_CHECK_CUDA(cudaGetLastError());
@@ -304,6 +365,39 @@ extern "C" kvf_status kvf_restore_batch(const kvf_restore_unit* units,
       if (!groups[v][dt].empty()) {
         kvf_status st = v == kBand ? launch_restore_band(groups[v][dt], dt, s)
                                    : launch_group(groups[v][dt], v, dt, s);
+        if (st != KVF_OK) return st;
+      }
+  return KVF_OK;
+}
+
+extern "C" kvf_status kvf_restore_batch_heads(const kvf_restore_unit* units, int32_t n_units,
+                                              int32_t head_lo, int32_t n_heads,
+                                              int32_t n_windows, int64_t window_stride,
+                                              int32_t raw_samples, void* stream) {
+  if (n_units < 0 || (n_units > 0 && units == nullptr))
+    KVF_FAIL(KVF_EINVAL, "bad unit array");
+  std::vector<kvf_restore_unit> groups[17][4];
+  for (int32_t k = 0; k < n_units; ++k) {
+    kvf_status st = check_unit(units[k]);
+    if (st != KVF_OK) return st;
+    if (head_lo < 0 || n_heads < 1 || n_windows < 1 ||
+        head_lo + (int64_t)n_windows * n_heads > units[k].plan.H)
+      KVF_FAIL(KVF_EINVAL, "head windows [%d, %lld) outside %d heads", head_lo,
+               (long long)head_lo + (long long)n_windows * n_heads, units[k].plan.H);
+    if (raw_samples && units[k].dst.dtype != KVF_I8)
+      KVF_FAIL(KVF_EINVAL, "raw samples need an int8 destination");
+    if (units[k].n_frames == 0) continue;
+    // the fast kernel when its conditions hold for the local cache, else the
+    // one-thread-per-sample kernel (tile rows narrower than 8 channels too)
+    groups[restore_variant(units[k])][units[k].dst.dtype].push_back(units[k]);
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const HeadWindow hw{head_lo, head_lo + n_windows * n_heads, n_heads, raw_samples ? 1 : 0,
+                      window_stride, true};
+  for (int v = 0; v < 17; ++v)
+    for (int dt = 0; dt < 4; ++dt)
+      if (!groups[v][dt].empty()) {
+        kvf_status st = launch_group(groups[v][dt], v, dt, s, hw);
         if (st != KVF_OK) return st;
       }
   return KVF_OK;

@@ -199,7 +199,10 @@ def _oracle_chunk(T, lay, res, seed, gs=128, F=4):
                                  (4, 8, 2, 2, 4, 2),
                                  # 512- and 256-channel slots: 2 / 4 items side by side per warp
                                  (4, 128, 1, 4, 1, 128), (4, 128, 2, 2, 8, 16),
-                                 (2, 128, 1, 2, 1, 128), (2, 128, 2, 1, 16, 8)])
+                                 (2, 128, 1, 2, 1, 128), (2, 128, 2, 1, 16, 8),
+                                 # 128-channel slots (a tensor-parallel head shard):
+                                 # 8 items side by side per warp
+                                 (1, 128, 1, 1, 1, 128), (2, 64, 2, 1, 8, 8)])
 @pytest.mark.parametrize("dtype", [torch.int8, torch.bfloat16, torch.float16, torch.float32])
 def test_restore_paged_matches_oracle(lay, dtype):
     H, D = lay[0], lay[1]
@@ -635,3 +638,58 @@ def test_all_tilings_32x128_pack_and_restore():
         assert np.array_equal(fr.cpu().numpy(), want), cfg
         back = L.disassemble_frames(fr, plan)
         assert np.array_equal(back.cpu().numpy(), v.reshape(T, 3, H * D)), cfg
+
+
+@pytest.mark.parametrize("lay", [(8, 128, 1, 8, 1, 128), (8, 128, 8, 1, 1, 128),
+                                 (8, 128, 2, 4, 16, 8), (8, 128, 1, 8, 128, 1)])
+def test_restore_head_window_matches_oracle(lay):
+    """kvf_restore_batch_heads: heads [2, 6) of every slot into a 4-head cache
+    (bf16, dequantised) and, as raw samples, into an int8 buffer; both against
+    the oracle.  (1, 8, 128, 1) has 1-channel tile rows: the per-sample kernel."""
+    H, D = lay[0], lay[1]
+    T, res, gs, lo, nh = 333, "R480", 128, 2, 4
+    x, v, s, frames = _oracle_chunk(T, lay, res, seed=9, gs=gs)
+    plan = L.plan_inter_frame(T, res, L.LayoutConfig(*lay), 4)
+    fr = torch.from_numpy(frames).cuda()
+    sc = torch.from_numpy(s).cuda()
+    deq = ref.dequantize(v, s, gs).reshape(T, 3, H, D)
+    for dtype, raw in ((torch.bfloat16, 0), (torch.int8, 1)):
+        out = torch.zeros((3, T, nh, D), dtype=dtype, device="cuda")
+        dst = _lib.kvf_paged()
+        for p in range(3):
+            dst.layer[p] = out[p].data_ptr()
+        dst.block_table = None
+        dst.block_size = 1
+        dst.dtype = {torch.bfloat16: _lib.KVF_BF16, torch.int8: _lib.KVF_I8}[dtype]
+        dst.block_stride = dst.slot_stride = nh * D
+        dst.head_stride = D
+        dst.token_base = 0
+        u = make_restore_unit(fr, plan, sc, dst, gs)
+        _lib.call("kvf_restore_batch_heads", (_lib.kvf_restore_unit * 1)(u), 1, lo, nh, 1, 0, raw,
+                  None)
+        torch.cuda.synchronize()
+        got = out.permute(1, 0, 2, 3).cpu()
+        if raw:
+            want = (v.reshape(T, 3, H, D)[:, :, lo:lo + nh].astype(np.int16) + 128).astype(np.uint8)
+            assert np.array_equal(got.numpy().view(np.uint8), want)
+        else:
+            want = torch.from_numpy(np.ascontiguousarray(deq[:, :, lo:lo + nh])).to(dtype)
+            assert torch.equal(got, want)
+    # all heads in two windows of 4: window w at +w * (3*T*4*D) of an int8 buffer
+    buf = torch.zeros((2, 3, T, 4, D), dtype=torch.int8, device="cuda")
+    dst = _lib.kvf_paged()
+    for p in range(3):
+        dst.layer[p] = buf[0, p].data_ptr()
+    dst.block_table, dst.block_size, dst.dtype = None, 1, _lib.KVF_I8
+    dst.block_stride = dst.slot_stride = 4 * D
+    dst.head_stride, dst.token_base = D, 0
+    u = make_restore_unit(fr, plan, None, dst, gs)
+    _lib.call("kvf_restore_batch_heads", (_lib.kvf_restore_unit * 1)(u), 1, 0, 4, 2,
+              3 * T * 4 * D, 0, None)
+    torch.cuda.synchronize()
+    codes = v.reshape(T, 3, H, D)
+    for w in range(2):
+        assert np.array_equal(buf[w].permute(1, 0, 2, 3).cpu().numpy(), codes[:, :, 4 * w:4 * w + 4])
+    with pytest.raises(ValueError):
+        _lib.call("kvf_restore_batch_heads", (_lib.kvf_restore_unit * 1)(u), 1, 6, 4, 1, 0, 0,
+                  None)

@@ -150,3 +150,13 @@ def test_two_rank_gloo_sharded_restore_equals_single_process():
     assert n_slots == world * 2 * T * LAYERS
     assert ms == 2.5                                   # max over ranks of 1.5 + rank
     assert total == sum(u.elements(H, D) for u in units)
+
+
+def test_head_window():
+    from paper_2602_09725_b200 import shard
+    assert [shard.head_window(8, r, 4) for r in range(4)] == [(0, 2), (2, 2), (4, 2), (6, 2)]
+    assert shard.head_window(8, 0, 1) == (0, 8)
+    with pytest.raises(ValueError):
+        shard.head_window(8, 0, 3)
+    with pytest.raises(ValueError):
+        shard.head_window(8, 2, 2)
