@@ -1,5 +1,5 @@
-"""GPU stress: repeat kvf_pack_batch (KVF_PACK_MODE selects the schedule) many times per config,
-count mismatches vs the oracle."""
+"""GPU stress: repeat kvf_pack_batch_ex (argv[2]: schedule, 0 auto / 1 two-pass /
+2 single read) many times per config, count mismatches vs the oracle."""
 import os
 import sys
 import time
@@ -15,6 +15,7 @@ from oracle import ref  # noqa: E402
 from paper_2602_09725_b200 import _dev, _lib, layout as L  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+schedule = int(sys.argv[2]) if len(sys.argv) > 2 else _lib.KVF_PACK_AUTO
 H, D, gs = 8, 128, 128
 for res, lay, T, Lyr, chunks in [
         ("R240", (8, 128, 1, 8, 1, 128), 700, 5, [(0, 400), (400, 300)]),
@@ -56,7 +57,8 @@ for res, lay, T, Lyr, chunks in [
                 u.frames = _dev.surface_of(fr)
                 units.append(u)
                 outs.append((trip, T0, fr, sc, am))
-        _lib.call("kvf_pack_batch", (_lib.kvf_pack_unit * len(units))(*units), len(units), None)
+        _lib.call("kvf_pack_batch_ex", (_lib.kvf_pack_unit * len(units))(*units), len(units),
+                  schedule, 0, None)
         torch.cuda.synchronize()
         for trip, T0, fr, sc, am in outs:
             s, fd = want[(trip, T0)]
