@@ -46,8 +46,7 @@ def main():
     ref_frames = [f.clone() for f in w.frames]
     ref_scales = [x.clone() for x in w.scales]
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
-    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO,
-             "chain": _lib.KVF_PACK_CHAIN}
+    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO}
     for x in filter(None, a.schedules.split(",")):
         nm, _, prm = x.partition(":")
         configs.append((names[nm], int(prm or 0)))
@@ -72,7 +71,7 @@ def main():
         per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps))
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
-        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "chain"}[sched]
+        sname = {0: "auto", 1: "two_pass", 2: "single_read"}[sched]
         print(json.dumps({"schedule": sname,
                           "cluster": slab, "ms_median": round(med, 4),
                           "ms_min": round(per[0], 4), "achieved_gbs": round(ach, 1),
