@@ -9,6 +9,7 @@ scales are bit-identical.  One JSON line per schedule.
 """
 import argparse
 import json
+import time
 import os
 import sys
 
@@ -28,8 +29,9 @@ def main():
     ap.add_argument("--layout", default="identity")
     ap.add_argument("--res", default="R1080")
     ap.add_argument("--schedules", default="single_read",
-                    help="comma list of single_read[:cluster] / auto")
+                    help="comma list of single_read[:cluster] / multi[:param] / auto")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of the call")
     a = ap.parse_args()
     args = argparse.Namespace(model=a.model, tokens=a.tokens, layout=a.layout, res=a.res, page=16,
                               requests=1, shard="balanced")
@@ -37,19 +39,33 @@ def main():
     w = bench.Workload(args, dev)
     s = torch.cuda.current_stream()
 
-    def run(sched, slab):
+    def call(sched, slab):
         _lib.call("kvf_pack_batch_ex", w._pack_arr, len(w.pack_units), sched, slab,
-                  _dev.stream_ptr(s))
+                  _dev.stream_ptr(torch.cuda.current_stream()))
+
+    graphs = {}
+
+    def run(sched, slab):
+        if not a.graph:
+            return call(sched, slab)
+        if (sched, slab) not in graphs:   # captured once, replayed per step
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                call(sched, slab)
+            graphs[(sched, slab)] = g
+        graphs[(sched, slab)].replay()
 
     run(_lib.KVF_PACK_TWO_PASS, 0)
     torch.cuda.synchronize()
     ref_frames = [f.clone() for f in w.frames]
     ref_scales = [x.clone() for x in w.scales]
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
-    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO}
+    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO,
+             "multi": _lib.KVF_PACK_MULTI_STREAM}
     for x in filter(None, a.schedules.split(",")):
         nm, _, prm = x.partition(":")
-        configs.append((names[nm], int(prm or 0)))
+        configs.append((names[nm], int(prm or "0", 0)))
     for sched, slab in configs:
         for f in w.frames:
             f.fill_(7)
@@ -64,18 +80,21 @@ def main():
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
         ev[0].record(s)
+        host = 0.0
         for k in range(a.steps):
+            h0 = time.perf_counter()
             run(sched, slab)
+            host += time.perf_counter() - h0
             ev[k + 1].record(s)
         torch.cuda.synchronize()
         per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps))
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
-        sname = {0: "auto", 1: "two_pass", 2: "single_read"}[sched]
+        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "multi"}[sched]
         print(json.dumps({"schedule": sname,
                           "cluster": slab, "ms_median": round(med, 4),
-                          "ms_min": round(per[0], 4), "achieved_gbs": round(ach, 1),
-                          "frac": round(ach / 6558.7, 4), "bit_exact": ok,
+                          "ms_min": round(per[0], 4), "host_ms": round(host * 1e3 / a.steps, 4), "achieved_gbs": round(ach, 1),
+                          "frac": round(ach / 6558.7, 4), "bit_exact": ok, "graph": a.graph,
                           "model": a.model, "tokens": a.tokens, "layout": a.layout}), flush=True)
 
 
