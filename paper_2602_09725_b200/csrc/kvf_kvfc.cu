@@ -28,28 +28,32 @@ namespace {
 using namespace rc;
 
 // Payload bytes through a 64-bit window: `win` holds the 8 bytes at [wa, wa+8),
-// the next byte is at `a` with a - wa < 4 at every symbol start.  A refill
-// shifts in the word prefetched one refill earlier (`nxt`), so the load never
-// sits on the decode chain.  Loads use clamped in-bounds addresses and bytes
-// at or past the end read as 0 (fk/rangecoder.py:158,181: data[pos] if pos < n).
+// the next byte is at `a` with a - wa < 4 at every symbol start.  Positions are
+// 32-bit byte offsets from the stream's first aligned word (`org`), so the
+// window arithmetic on the decode chain is 32-bit.  A refill shifts in the word
+// prefetched one refill earlier (`nxt`), so the load never sits on the decode
+// chain; the word is masked as it is shifted in, so every byte of `win` at or
+// past the end is already 0 (fk/rangecoder.py:158,181: data[pos] if pos < n)
+// and take() needs no bounds test.  Loads use clamped in-bounds addresses.
 // FED: the payload is still being copied in (kvf_rc_decode_fed): a word is
 // read only once the pieces holding it landed (`ready` pieces of the stream's
 // copy segment, acquire).  Pieces end on 128-byte lines, so a line a thread
 // caches in L1 never holds bytes that land later.
 template <bool FED>
 struct ByteWindow {
+  const uint8_t* org;          // the payload's first byte rounded down to 4
   uint64_t win;
-  uintptr_t wa, a, end, last;  // last = the last aligned word holding payload bytes
+  uint32_t wa, a, end, last;   // offsets from org; last = the last word holding payload
   uint32_t nxt;                // raw word at wa + 8 (loaded one refill ahead)
-  bool nxt_ok;                 // wa + 8 < end: otherwise it reads as 0
-  // FED only: bytes below `avail` have landed; segment start, piece size, counter
+  // FED only: bytes below `avail` (absolute) have landed; segment start, piece size, counter
   uintptr_t avail, seg0;
   uint32_t piece;
   const uint32_t* ready;
-  __device__ __forceinline__ void await(uintptr_t need) {  // bytes below need landed
+  __device__ __forceinline__ void await(uint32_t need) {  // bytes below offset need landed
     if (!FED) return;
     need = need < end ? need : end;
-    if (avail < need) avail = await_slow(ready, seg0, piece, need);
+    const uintptr_t abs_need = reinterpret_cast<uintptr_t>(org) + need;
+    if (avail < abs_need) avail = await_slow(ready, seg0, piece, abs_need);
   }
   // Polls the segment's landed-piece count until `need` is covered (out of
   // line: the decode loop only carries the compare).
@@ -63,41 +67,39 @@ struct ByteWindow {
       __nanosleep(256);
     }
   }
-  __device__ __forceinline__ uint32_t ld(uintptr_t w) const {
-    return __ldg(reinterpret_cast<const uint32_t*>(w));
+  // word at offset w with the bytes at or past the end zeroed
+  __device__ __forceinline__ uint32_t masked(uint32_t word, uint32_t w) const {
+    const int32_t v = (int32_t)(end - w);  // payload bytes in the word
+    return v >= 4 ? word : (v <= 0 ? 0u : word & ((1u << (8 * v)) - 1u));
   }
-  __device__ __forceinline__ uint32_t load(uintptr_t w) {  // in bounds, unmasked
-    const uintptr_t x = w < end ? w : last;
+  __device__ __forceinline__ uint32_t load(uint32_t w) {  // clamped in bounds, masked
+    const uint32_t x = w < end ? w : last;
     await(x + 4);
-    return ld(x);
+    return masked(__ldg(reinterpret_cast<const uint32_t*>(org + x)), w);
   }
   __device__ __forceinline__ void init(const uint8_t* p, uint32_t n) {
-    a = reinterpret_cast<uintptr_t>(p);
+    org = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3));
+    a = (uint32_t)(p - org);
     end = a + n;
-    wa = a & ~uintptr_t(3);
-    last = n ? (end - 1) & ~uintptr_t(3) : wa;
+    wa = 0;
+    last = n ? (end - 1) & ~3u : 0u;
     if (n == 0) {  // every byte reads as 0; never dereference
       win = 0;
       nxt = 0;
-      nxt_ok = false;
       end = 0;
       return;
     }
-    const uint32_t w0 = load(wa), w1 = wa + 4 < end ? load(wa + 4) : 0u;
-    win = (uint64_t)w0 | ((uint64_t)w1 << 32);
-    nxt = load(wa + 8);
-    nxt_ok = wa + 8 < end;
+    win = (uint64_t)load(0) | ((uint64_t)load(4) << 32);
+    nxt = load(8) ;
   }
   __device__ __forceinline__ uint32_t peek() const {  // byte at a (a - wa < 8)
-    return a < end ? (uint32_t)(win >> (8 * (a - wa))) & 0xFFu : 0u;
+    return (uint32_t)(win >> (8 * (a - wa))) & 0xFFu;
   }
   // The next n <= 3 bytes as a big-endian number (first byte most significant;
   // bytes at or past the end are 0); advances a.  Needs a - wa < 4.
   __device__ __forceinline__ uint32_t take(uint32_t n) {
-    uint32_t w = (uint32_t)(win >> (8 * (a - wa)));           // bytes a.. a+3, little-endian
-    const uintptr_t valid = end > a ? end - a : 0;            // bytes before the end
-    w = valid >= 4 ? w : w & ((1u << (8 * (uint32_t)valid)) - 1u);
-    const uint32_t be = __byte_perm(w, 0u, 0x0123);           // byte a in bits 24..31
+    const uint32_t w = (uint32_t)(win >> (8 * (a - wa)));  // bytes a.. a+3, little-endian
+    const uint32_t be = __byte_perm(w, 0u, 0x0123);         // byte a in bits 24..31
     a += n;
     return n ? be >> (32 - 8 * n) : 0u;
   }
@@ -105,18 +107,18 @@ struct ByteWindow {
   // load it came from had a whole symbol to land) and prefetch the next one.
   __device__ __forceinline__ void refill() {
     const bool go = a - wa >= 4;
-    const uint64_t shifted = (win >> 32) | ((uint64_t)(nxt_ok ? nxt : 0u) << 32);
+    const uint64_t shifted = (win >> 32) | ((uint64_t)masked(nxt, wa + 8) << 32);
     win = go ? shifted : win;
     wa = go ? wa + 4 : wa;
     // predicated load straight into `nxt`: no instruction consumes it until
     // the next refill, so its latency never stalls the decode chain
-    const uintptr_t src = wa + 8 < end ? wa + 8 : last;
+    const uint32_t x = wa + 8 < end ? wa + 8 : last;
+    const uint8_t* src = org + x;
     // (FED: the block-level wait of rc_decode_kernel covers this prefetch)
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.global.nc.u32 %0, [%1];\n}"
         : "+r"(nxt)
         : "l"(src), "r"((uint32_t)(go && end != 0)));
-    nxt_ok = go ? wa + 8 < end : nxt_ok;
   }
 };
 
