@@ -337,7 +337,7 @@ def _decode_batch(streams, out, stream, ranges, indices, max_parts, staged):
 # itself, piece-major, so every plane starts after its first piece instead of
 # after the batch's last copy.
 _FED_MIN_SYMBOLS = 98_304
-_FED_PIECE = 16 * 1024
+_FED_PIECE = 4 * 1024
 _FED_COPY_CTAS = 128
 
 

@@ -139,7 +139,7 @@ __device__ __forceinline__ void fed_mark(int, int) {}
 // host -> device over PCIe (16-byte loads of mapped pinned memory), piece r of
 // every segment before piece r+1 of any, and count each segment's landed
 // pieces in ready[] (in order, release).
-constexpr uint32_t kFedBlock = 512;  // symbols decoded per landed-bytes check
+constexpr uint32_t kFedBlock = 64;  // symbols decoded per landed-bytes check
 
 struct FeedArgs {
   const kvf_feed_seg* segs;

@@ -19,6 +19,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--res", default="R1080")
     ap.add_argument("--quick", action="store_true", help="one fed decode (for ncu)")
+    ap.add_argument("--ctas", type=lambda x: [int(v) for v in x.split(",")], default=[32, 128, 512])
+    ap.add_argument("--pieces", type=lambda x: [int(v) for v in x.split(",")], default=[16384, 65536])
+    ap.add_argument("--copy-only", type=lambda x: [int(v) for v in x.split(",") if v],
+                    default=[32, 128, 512])
     a = ap.parse_args()
     args = argparse.Namespace(model="llama3-8b", tokens=32768, layout="identity", res=a.res,
                               page=16, requests=1, shard="balanced")
@@ -47,8 +51,8 @@ def main():
     codec._FED_MIN_SYMBOLS = 1 << 40
     run("part pipeline")
     codec._FED_MIN_SYMBOLS = base_min
-    for ctas in (32, 128, 512):
-        for piece in (16384, 65536):
+    for ctas in a.ctas:
+        for piece in a.pieces:
             codec._FED_COPY_CTAS, codec._FED_PIECE = ctas, piece
             run(f"fed copy_ctas={ctas} piece={piece}")
     # the copy side alone: a fed launch whose decoders have nothing to decode
@@ -60,7 +64,7 @@ def main():
         rc["n_symbols"] = 0
         return rc, flat[:0], ch[:0]
     codec._part_descriptors = no_decode
-    for ctas in (32, 128, 512):
+    for ctas in a.copy_only:
         codec._FED_COPY_CTAS, codec._FED_PIECE = ctas, 16384
         codec.decode_batch(streams, out=frames)
         torch.cuda.synchronize()
