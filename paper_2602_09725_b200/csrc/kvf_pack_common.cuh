@@ -368,6 +368,62 @@ __device__ __forceinline__ void pack_items(const PackUnitDev& U, int p,
         }
       }
     }
+  } else if constexpr (SUB == 1) {
+    // Software pipeline: the loads of item it+1 are in flight while item it is
+    // quantised and stored.  The item addresses are located lane-parallel:
+    // lane l locates round r0 + l once for the warp (instead of every lane
+    // locating every round) and round it takes them with two shuffles.
+    const int lane = threadIdx.x & 31;
+    uint8_t* my_dst = nullptr;
+    const char* my_src = nullptr;
+    auto fill = [&](int r0) {
+      const int q = item0 + (r0 + lane) * stride;
+      my_dst = nullptr;
+      my_src = nullptr;
+      if (r0 + lane < rounds && q < end) locate(q, my_dst, my_src);
+    };
+    auto get = [&](int it, uint8_t*& d, const char*& sp) {
+      d = reinterpret_cast<uint8_t*>(__shfl_sync(
+          0xffffffffu, (unsigned long long)reinterpret_cast<uintptr_t>(my_dst), it & 31));
+      sp = reinterpret_cast<const char*>(__shfl_sync(
+          0xffffffffu, (unsigned long long)reinterpret_cast<uintptr_t>(my_src), it & 31));
+    };
+    Raw8<SRC> cur[VL], nxt[VL];
+    uint8_t* dst_cur = nullptr;
+    const char* src_cur = nullptr;
+    const int n_it = rounds;  // warp-uniform
+    fill(0);
+    get(0, dst_cur, src_cur);
+    if (src_cur)
+#pragma unroll
+      for (int k = 0; k < VL; ++k) cur[k] = load_raw8<SRC>(src_cur + L.in_off[k], ld);
+    for (int it = 0; it < n_it; ++it) {
+      uint8_t* dst_nxt = nullptr;
+      const char* src_nxt = nullptr;
+      if (it + 1 < n_it) {
+        if (((it + 1) & 31) == 0) fill(it + 1);
+        get(it + 1, dst_nxt, src_nxt);
+        if (src_nxt)
+#pragma unroll
+          for (int k = 0; k < VL; ++k) nxt[k] = load_raw8<SRC>(src_nxt + L.in_off[k], ld);
+      }
+      if (dst_cur != nullptr) {
+#pragma unroll
+        for (int k = 0; k < VL; ++k) {
+          uint2 out = make_uint2(0x80808080u, 0x80808080u);
+          if (src_cur) {
+            float x[8];
+            raw8_to_float<SRC>(cur[k], x);
+            out = quantize8<kRange>(x, L.s[k], L.inv[k]);
+          }
+          st_v2(dst_cur + L.tile_off[k], out);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < VL; ++k) cur[k] = nxt[k];
+      dst_cur = dst_nxt;
+      src_cur = src_nxt;
+    }
   } else {
     // Software pipeline: the loads of item it+1 are in flight while item it is
     // quantised and stored.
