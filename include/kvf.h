@@ -209,14 +209,11 @@ kvf_status kvf_pack_batch(const kvf_pack_unit* units, int32_t n_units,
 typedef enum kvf_pack_schedule {
   KVF_PACK_AUTO = 0,        /* the fastest measured on this build */
   KVF_PACK_TWO_PASS = 1,    /* absmax kernel, then frames kernel: reads the source twice */
-  KVF_PACK_SINGLE_READ = 2, /* one HBM read: clusters of 8 (or 16) CTAs own whole
+  KVF_PACK_SINGLE_READ = 2  /* one HBM read: clusters of 8 (or 16) CTAs own whole
                                (unit, plane, group) sub-units, stream them through shared
                                memory with TMA, exchange the maxima through distributed
                                shared memory and re-read from L2.  Slower than two-pass on
                                B200 */
-  KVF_PACK_MULTI_STREAM = 3 /* one HBM read: a fold kernel and a quantise kernel per
-                               (unit, plane), spread over several library-owned streams
-                               forked from and joined back into the caller's stream */
 } kvf_pack_schedule;
 
 /* kvf_pack_batch with an explicit schedule.  `param` (single read only): CTAs

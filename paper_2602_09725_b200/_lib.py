@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libkvf.so")
 
 KVF_OK, KVF_EINVAL, KVF_ECUDA, KVF_EUNSUPPORTED, KVF_EDECODE = range(5)
 KVF_BF16, KVF_F16, KVF_F32, KVF_I8 = range(4)
-KVF_PACK_AUTO, KVF_PACK_TWO_PASS, KVF_PACK_SINGLE_READ, KVF_PACK_MULTI_STREAM = range(4)
+KVF_PACK_AUTO, KVF_PACK_TWO_PASS, KVF_PACK_SINGLE_READ = range(3)
 KVF_MAX_UNITS = 128
 ABI_VERSION = 1
 

@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libkvf.so")
 
-SOURCES = ["kvf_api.cu", "kvf_restore.cu", "kvf_pack.cu", "kvf_pack_stream.cu", "kvf_pack_multi.cu", "kvf_band.cu", "kvf_kvfc.cu",
+SOURCES = ["kvf_api.cu", "kvf_restore.cu", "kvf_pack.cu", "kvf_pack_stream.cu", "kvf_band.cu", "kvf_kvfc.cu",
            "kvf_kvfc_enc.cu", "kvf_kvfc_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

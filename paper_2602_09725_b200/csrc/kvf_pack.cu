@@ -21,8 +21,6 @@ kvf_status launch_pack_stream(const std::vector<kvf_pack_unit>& units, int32_t d
                               int cluster, int probe, cudaStream_t s,
                               std::vector<kvf_pack_unit>* rest);
 bool pack_band_ok(const kvf_pack_unit& u);
-kvf_status launch_pack_multi(const std::vector<kvf_pack_unit>& units, int vpl, int32_t dtype,
-                             int64_t param, cudaStream_t s, bool* launched);
 kvf_status launch_pack_band(const std::vector<kvf_pack_unit>& units, int32_t dtype,
                             cudaStream_t s);
 // pack group variants: 0 generic, 1..16 fast kernels (VPL), kBandBase + v =
@@ -324,11 +322,10 @@ kvf_status launch_phases(const std::vector<kvf_pack_unit>& units, int variant, i
 kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t schedule,
                int64_t param, cudaStream_t s) {
   if (n_units < 0 || (n_units > 0 && units == nullptr)) KVF_FAIL(KVF_EINVAL, "bad unit array");
-  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_MULTI_STREAM)
+  if (schedule < KVF_PACK_AUTO || schedule > KVF_PACK_SINGLE_READ)
     KVF_FAIL(KVF_EINVAL, "bad pack schedule %d", schedule);
   if (param < 0) KVF_FAIL(KVF_EINVAL, "negative schedule parameter");
   const bool single = schedule == KVF_PACK_SINGLE_READ && phases == (1 | 2 | 4 | 8);
-  const bool multi = schedule == KVF_PACK_MULTI_STREAM && phases == (1 | 2 | 4 | 8);
   std::vector<kvf_pack_unit> by_dtype[4];
   for (int32_t k = 0; k < n_units; ++k) {
     kvf_status st = check_unit(units[k]);
@@ -354,12 +351,6 @@ kvf_status run(const kvf_pack_unit* units, int32_t n_units, int phases, int32_t 
   for (int v = 0; v < kBandBase + 17; ++v)
     for (int dt = 0; dt < 4; ++dt)
       if (!groups[v][dt].empty()) {
-        if (multi && v >= 1 && v <= 16 && dt != KVF_I8) {
-          bool launched = false;
-          kvf_status st = launch_pack_multi(groups[v][dt], v, dt, param, s, &launched);
-          if (st != KVF_OK) return st;
-          if (launched) continue;
-        }
         kvf_status st = launch_phases(groups[v][dt], v, dt, phases, s);
         if (st != KVF_OK) return st;
       }

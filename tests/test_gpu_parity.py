@@ -68,13 +68,13 @@ def test_assemble_disassemble_bit_exact(golden):
 
 # pack schedules (include/kvf.h kvf_pack_schedule): every one must give the
 # oracle's bytes; single_read with 8- (default) and 16-CTA clusters
-SCHEDULES = ["two_pass", "single_read", "single_read:16", "multi", "multi:0x112", "auto"]
+SCHEDULES = ["two_pass", "single_read", "single_read:16", "auto"]
 
 
 def _pack(arr, n, mode):
     name, _, param = mode.partition(":")
     sched = {"auto": _lib.KVF_PACK_AUTO, "two_pass": _lib.KVF_PACK_TWO_PASS,
-             "single_read": _lib.KVF_PACK_SINGLE_READ, "multi": _lib.KVF_PACK_MULTI_STREAM}[name]
+             "single_read": _lib.KVF_PACK_SINGLE_READ}[name]
     _lib.call("kvf_pack_batch_ex", arr, n, sched, int(param or "0", 0), None)
 
 

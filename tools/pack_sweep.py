@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--layout", default="identity")
     ap.add_argument("--res", default="R1080")
     ap.add_argument("--schedules", default="single_read",
-                    help="comma list of single_read[:cluster] / multi[:param] / auto")
+                    help="comma list of single_read[:cluster] / auto")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of the call")
     a = ap.parse_args()
@@ -61,8 +61,7 @@ def main():
     ref_frames = [f.clone() for f in w.frames]
     ref_scales = [x.clone() for x in w.scales]
     configs = [(_lib.KVF_PACK_TWO_PASS, 0)]
-    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO,
-             "multi": _lib.KVF_PACK_MULTI_STREAM}
+    names = {"single_read": _lib.KVF_PACK_SINGLE_READ, "auto": _lib.KVF_PACK_AUTO}
     for x in filter(None, a.schedules.split(",")):
         nm, _, prm = x.partition(":")
         configs.append((names[nm], int(prm or "0", 0)))
@@ -90,7 +89,7 @@ def main():
         per = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps))
         med = per[len(per) // 2]
         ach = 3.0 * w.elems / (med * 1e-3) / 1e9
-        sname = {0: "auto", 1: "two_pass", 2: "single_read", 3: "multi"}[sched]
+        sname = {0: "auto", 1: "two_pass", 2: "single_read"}[sched]
         print(json.dumps({"schedule": sname,
                           "cluster": slab, "ms_median": round(med, 4),
                           "ms_min": round(per[0], 4), "host_ms": round(host * 1e3 / a.steps, 4), "achieved_gbs": round(ach, 1),
