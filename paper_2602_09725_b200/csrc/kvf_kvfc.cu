@@ -39,33 +39,47 @@ using namespace rc;
 // read only once the pieces holding it landed (`ready` pieces of the stream's
 // copy segment, acquire).  Pieces end on 128-byte lines, so a line a thread
 // caches in L1 never holds bytes that land later.
+// FED: what only the landed-bytes poll needs, kept in shared memory (one per
+// thread) so that the decode loop carries a single 32-bit bound: with these
+// fields live in registers across the loop the FED kernel ran 14% slower.
+struct FedCold {
+  const uint32_t* ready;  // landed-piece count of the stream's copy segment
+  uintptr_t seg0;         // the segment's piece origin (its first 128-byte line)
+  uintptr_t org;          // the window's origin
+  uint32_t piece;         // piece bytes
+  uint32_t pad_;
+};
+
+__shared__ FedCold g_fed_cold[kDecThreads];  // FED kernels: one per decoder thread
+
+// Polls until the bytes below offset `need` have landed; returns the landed
+// offset (out of line: the decode loop only carries the compare).
+__device__ __noinline__ uint32_t fed_poll(uint32_t need) {
+  const FedCold* c = &g_fed_cold[threadIdx.x];
+  const uintptr_t abs_need = c->org + need;
+  for (;;) {
+    uint32_t r;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(c->ready) : "memory");
+    const uintptr_t av = c->seg0 + (uintptr_t)r * c->piece;
+    if (av >= abs_need) {
+      const uintptr_t off = av - c->org;
+      return off > 0xFFFFFFFFu ? 0xFFFFFFFFu : (uint32_t)off;
+    }
+    __nanosleep(256);
+  }
+}
+
 template <bool FED>
 struct ByteWindow {
   const uint8_t* org;          // the payload's first byte rounded down to 4
   uint64_t win;
   uint32_t wa, a, end, last;   // offsets from org; last = the last word holding payload
   uint32_t nxt;                // raw word at wa + 8 (loaded one refill ahead)
-  // FED only: bytes below `avail` (absolute) have landed; segment start, piece size, counter
-  uintptr_t avail, seg0;
-  uint32_t piece;
-  const uint32_t* ready;
+  uint32_t lim;                // FED: the bytes below offset lim have landed
   __device__ __forceinline__ void await(uint32_t need) {  // bytes below offset need landed
     if (!FED) return;
     need = need < end ? need : end;
-    const uintptr_t abs_need = reinterpret_cast<uintptr_t>(org) + need;
-    if (avail < abs_need) avail = await_slow(ready, seg0, piece, abs_need);
-  }
-  // Polls the segment's landed-piece count until `need` is covered (out of
-  // line: the decode loop only carries the compare).
-  static __device__ __noinline__ uintptr_t await_slow(const uint32_t* ready, uintptr_t seg0,
-                                                      uint32_t piece, uintptr_t need) {
-    for (;;) {
-      uint32_t r;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(ready) : "memory");
-      const uintptr_t av = seg0 + (uintptr_t)r * piece;
-      if (av >= need) return av;
-      __nanosleep(256);
-    }
+    if (need > lim) lim = fed_poll(need);
   }
   // word at offset w with the bytes at or past the end zeroed
   __device__ __forceinline__ uint32_t masked(uint32_t word, uint32_t w) const {
@@ -139,7 +153,9 @@ __device__ __forceinline__ void fed_mark(int, int) {}
 // host -> device over PCIe (16-byte loads of mapped pinned memory), piece r of
 // every segment before piece r+1 of any, and count each segment's landed
 // pieces in ready[] (in order, release).
-constexpr uint32_t kFedBlock = 64;  // symbols decoded per landed-bytes check
+// symbols decoded per landed-bytes check: 64 needs 528 bytes landed ahead (128
+// and 256 made the decoders wait near the copy frontier: 199 / 286 ms on C2)
+constexpr uint32_t kFedBlock = 64;
 
 struct FeedArgs {
   const kvf_feed_seg* segs;
@@ -207,12 +223,14 @@ __global__ void __launch_bounds__(kDecThreads)
   model_init(m, P);
   uint32_t total = 256, low = 0, rng = 0xFFFFFFFFu, code = 0;
   ByteWindow<FED> bw;
-  if (FED) {
+  if constexpr (FED) {
     const int k = F.seg_of[sidx];
-    bw.seg0 = reinterpret_cast<uintptr_t>(F.segs[k].dst) & ~uintptr_t(127);  // piece origin
-    bw.piece = (uint32_t)F.piece;
-    bw.ready = F.ready + k;
-    bw.avail = 0;
+    FedCold& c = g_fed_cold[tid];
+    c.seg0 = reinterpret_cast<uintptr_t>(F.segs[k].dst) & ~uintptr_t(127);  // piece origin
+    c.piece = (uint32_t)F.piece;
+    c.ready = F.ready + k;
+    c.org = reinterpret_cast<uintptr_t>(st.payload) & ~uintptr_t(3);  // = bw.org (init)
+    bw.lim = 0;
   }
   if (FED) fed_mark(sidx, 0);
   bw.init(st.payload, (uint32_t)st.len);
@@ -618,8 +636,11 @@ extern "C" kvf_status kvf_rc_decode_fed(const kvf_rc_stream* d_streams, int32_t 
   KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   KVF_CHECK_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   const int want_per_sm = std::max(1, (grid + sms - 1) / sms);
+  cudaFuncAttributes fa{};
+  KVF_CHECK_CUDA(cudaFuncGetAttributes(&fa, rc_decode_kernel<true>));
+  // per CTA: dynamic + static shared memory + the 1 KB the hardware reserves
   size_t smem = (size_t)kDecThreads * 256 * sizeof(uint16_t);
-  smem = std::max(smem, (size_t)(smem_sm / want_per_sm) - 2048);
+  smem = std::max(smem, (size_t)(smem_sm / want_per_sm) - fa.sharedSizeBytes - 1024 - 512);
   smem = std::min<size_t>(smem, 200 * 1024);
   KVF_CHECK_CUDA(cudaFuncSetAttribute(rc_decode_kernel<true>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
