@@ -136,8 +136,10 @@ struct ByteWindow {
     // When that word starts a 128-byte line, pull the line two ahead into L1:
     // otherwise the first load of each line misses to DRAM, longer than one
     // symbol, and the next refill waits for it (8% of the decode's stalls).
+    // FED: only a line that has wholly landed (below lim; pieces end on lines),
+    // so L1 never holds bytes that land later.
     const bool line = go && ((uint32_t)reinterpret_cast<uintptr_t>(src) & 127u) == 0 &&
-                      x + 256 < end;
+                      (FED ? x + 384 <= lim : x + 256 < end);
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p prefetch.global.L1 [%0];\n}"
         :: "l"(src + 256), "r"((uint32_t)line));
