@@ -274,6 +274,21 @@ kvf_status kvf_kvfc_scan(const uint8_t* data, int64_t size, kvf_kvfc_info* info,
                          int64_t* bitmap_off, uint8_t* frame_type,
                          int32_t cap_frames, int32_t* bad_frame);
 
+/* kvf_kvfc_scan of n_streams streams in one call (replaces the reference's
+ * per-stream walk in decode_frames, fk/codec.py:164-208, for a batch).  With
+ * frame_base == NULL only the headers are read (info[j] filled).  Otherwise
+ * stream j's frames are written at frame index frame_base[j] of the flat
+ * arrays (entries 3*frame_base[j] .. of payload_off / payload_len /
+ * bitmap_off, frame_base[j] .. of frame_type), walked on up to n_threads host
+ * threads.  Errors as kvf_kvfc_scan, for the first failing stream in order:
+ * *bad_stream (-1 when none) and *bad_frame locate it. */
+kvf_status kvf_kvfc_scan_batch(const uint8_t* const* data, const int64_t* size,
+                               int32_t n_streams, kvf_kvfc_info* info,
+                               const int64_t* frame_base, int64_t* payload_off,
+                               int32_t* payload_len, int64_t* bitmap_off,
+                               uint8_t* frame_type, int32_t n_threads,
+                               int32_t* bad_stream, int32_t* bad_frame);
+
 /* One range-coded symbol stream (one plane of one frame). */
 typedef struct kvf_rc_stream {
   const uint8_t* payload;  /* device */

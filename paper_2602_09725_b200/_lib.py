@@ -165,6 +165,8 @@ _SIGNATURES = {
     "kvf_ar1_scan": (C.c_int, [_VP, C.c_int64, C.c_int64, C.c_int64, C.c_float, _VP]),
     "kvf_kvfc_scan": (C.c_int, [_VP, C.c_int64, C.POINTER(kvf_kvfc_info), _VP, _VP, _VP, _VP,
                                 C.c_int32, C.POINTER(C.c_int32)]),
+    "kvf_kvfc_scan_batch": (C.c_int, [_VP, _VP, C.c_int32, _VP, _VP, _VP, _VP, _VP, _VP,
+                                      C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "kvf_restore_batch_heads": (C.c_int, [C.POINTER(kvf_restore_unit), C.c_int32, C.c_int32,
                                           C.c_int32, C.c_int32, C.c_int64, C.c_int32, _VP]),
     "kvf_rc_decode": (C.c_int, [_VP, C.c_int32, _VP]),

@@ -123,30 +123,67 @@ class StreamIndex:
         _lib.check(st)
 
 
-_SCAN_POOL = None
-_SCAN_POOL_LOCK = threading.Lock()
+_SCAN_THREADS = 8  # host threads of the batched stream walk
 
 
 def index_streams(datas) -> list:
-    """StreamIndex of every stream, walked in parallel on host threads.
+    """StreamIndex of every stream: two kvf_kvfc_scan_batch calls (headers,
+    then the walk on host threads inside libkvf) instead of two ctypes calls
+    and four allocations per stream.
 
     The walk is a pointer chase through the stream (each plane's length word
-    gives the next position), one cache/TLB miss per plane, and kvf_kvfc_scan
-    runs without the GIL, so streams are spread over a small thread pool.
-    Errors are raised as by StreamIndex, for the first failing stream in order.
+    gives the next position), one cache/TLB miss per plane, so streams are
+    spread over threads.  Errors are raised as by StreamIndex, for the first
+    failing stream in order.
     """
-    global _SCAN_POOL
     datas = list(datas)
     if len(datas) < 4:
         return [StreamIndex(d) for d in datas]
-    with _SCAN_POOL_LOCK:
-        if _SCAN_POOL is None:
-            import concurrent.futures
-            import os
-            _SCAN_POOL = concurrent.futures.ThreadPoolExecutor(
-                max_workers=max(1, min(8, (os.cpu_count() or 2) // 2)),
-                thread_name_prefix="kvfc-scan")
-    return list(_SCAN_POOL.map(StreamIndex, datas))
+    lib = _lib.load()
+    n_st = len(datas)
+    views = [_host_view(d) for d in datas]
+    addr = np.array([v[0] for v in views], np.uint64)
+    size = np.array([v[1] for v in views], np.int64)
+    infos = (_lib.kvf_kvfc_info * n_st)()
+    bad_s, bad_f = C.c_int32(-1), C.c_int32(0)
+
+    def scan(base, po, pl, bo, ft):
+        ptr = (lambda a: C.c_void_p(a.ctypes.data) if a is not None else None)
+        return lib.kvf_kvfc_scan_batch(
+            C.c_void_p(addr.ctypes.data), C.c_void_p(size.ctypes.data), n_st, infos,
+            ptr(base), ptr(po), ptr(pl), ptr(bo), ptr(ft), _SCAN_THREADS,
+            C.byref(bad_s), C.byref(bad_f))
+
+    def fail(st):
+        if st == _lib.KVF_EDECODE:
+            raise DecodeError(lib.kvf_last_error().decode(), frame_index=bad_f.value)
+        _lib.check(st)
+
+    st = scan(None, None, None, None, None)
+    if st != _lib.KVF_OK:
+        fail(st)
+    n = np.array([infos[j].n_frames for j in range(n_st)], np.int64)
+    base = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+    total = int(base[-1])
+    po = np.zeros(3 * total, np.int64)
+    pl = np.zeros(3 * total, np.int32)
+    bo = np.zeros(3 * total, np.int64)
+    ft = np.zeros(max(total, 1), np.uint8)
+    st = scan(base, po, pl, bo, ft)
+    if st != _lib.KVF_OK:
+        fail(st)
+    out = []
+    for j in range(n_st):
+        ix = StreamIndex.__new__(StreamIndex)
+        b0, b1 = int(base[j]), int(base[j + 1])
+        inf = infos[j]
+        ix.n, ix.h, ix.w, ix.bitmap_len = inf.n_frames, inf.height, inf.width, inf.bitmap_len
+        ix.payload_off = po[3 * b0:3 * b1]
+        ix.payload_len = pl[3 * b0:3 * b1]
+        ix.bitmap_off = bo[3 * b0:3 * b1]
+        ix.frame_type = ft[b0:b1] if b1 > b0 else np.zeros(1, np.uint8)
+        out.append(ix)
+    return out
 
 
 class _PinnedStaging:

@@ -10,6 +10,11 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
+#include <atomic>
+#include <thread>
+#include <vector>
+
 #include "../../include/kvf.h"
 
 namespace kvf {
@@ -91,5 +96,65 @@ extern "C" kvf_status kvf_kvfc_scan(const uint8_t* data, int64_t size, kvf_kvfc_
     }
   }
   if (pos != size) return decode_error(bad_frame, (int32_t)n - 1, "trailing bytes");
+  return KVF_OK;
+}
+
+// Many streams: a header pass (frame_base == NULL: infos only) or the fill pass
+// over up to n_threads host threads, stream j's frames at frame_base[j] of the
+// flat arrays.  The walk is a pointer chase with one cache miss per plane, so
+// streams are spread over threads; one call replaces a Python-level loop of
+// two kvf_kvfc_scan calls per stream.  On an error the first failing stream
+// (in order) is walked again on the calling thread, so kvf_last_error()
+// describes it; *bad_stream / *bad_frame locate it.
+extern "C" kvf_status kvf_kvfc_scan_batch(const uint8_t* const* data, const int64_t* size,
+                                          int32_t n_streams, kvf_kvfc_info* info,
+                                          const int64_t* frame_base, int64_t* payload_off,
+                                          int32_t* payload_len, int64_t* bitmap_off,
+                                          uint8_t* frame_type, int32_t n_threads,
+                                          int32_t* bad_stream, int32_t* bad_frame) {
+  if (n_streams < 0 || (n_streams > 0 && (!data || !size || !info))) {
+    kvf::set_error("null argument");
+    return KVF_EINVAL;
+  }
+  if (bad_stream) *bad_stream = -1;
+  const bool fill = frame_base != nullptr;
+  if (fill && (!payload_off || !payload_len || !bitmap_off || !frame_type)) {
+    kvf::set_error("null output array");
+    return KVF_EINVAL;
+  }
+  std::vector<kvf_status> st(n_streams, KVF_OK);
+  auto walk = [&](int32_t j, int32_t* bad) -> kvf_status {
+    if (!fill) {  // header: a size query (KVF_EINVAL with info filled is success)
+      const kvf_status s = kvf_kvfc_scan(data[j], size[j], &info[j], nullptr, nullptr, nullptr,
+                                         nullptr, 0, bad);
+      return s == KVF_EINVAL && size[j] >= 12 ? KVF_OK : s;
+    }
+    const int64_t b = frame_base[j];
+    return kvf_kvfc_scan(data[j], size[j], &info[j], payload_off + 3 * b, payload_len + 3 * b,
+                         bitmap_off + 3 * b, frame_type + b, (int32_t)info[j].n_frames, bad);
+  };
+  const int32_t nt = std::max(1, std::min<int32_t>(fill ? n_threads : 1, n_streams));
+  std::atomic<int32_t> next(0);
+  auto worker = [&]() {
+    for (int32_t j; (j = next.fetch_add(1)) < n_streams;) {
+      int32_t bad = 0;
+      st[j] = walk(j, &bad);
+    }
+  };
+  if (nt == 1) {
+    worker();
+  } else {
+    std::vector<std::thread> pool;
+    for (int32_t t = 0; t < nt; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+  }
+  for (int32_t j = 0; j < n_streams; ++j) {
+    if (st[j] == KVF_OK) continue;
+    int32_t bad = 0;
+    const kvf_status s = walk(j, &bad);  // again on this thread: its error message
+    if (bad_stream) *bad_stream = j;
+    if (bad_frame) *bad_frame = bad;
+    return s;
+  }
   return KVF_OK;
 }

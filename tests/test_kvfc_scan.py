@@ -82,3 +82,31 @@ def test_empty_stream():
     with pytest.raises(DecodeError) as ei:
         StreamIndex(data + b"\x01")
     assert ei.value.frame_index == -1  # the reference reports frame n-1
+
+
+def test_batch_walk_equals_per_stream_walk():
+    """index_streams (kvf_kvfc_scan_batch, threaded) gives StreamIndex's arrays
+    for every stream, including empty and single-frame ones."""
+    from paper_2602_09725_b200.codec import index_streams
+    streams = [ref.encode_frames(cases.codec_frames(c), c["gop"]) for c in cases.CODEC_CASES]
+    streams += [struct.pack("<III", 0, 4, 4)] + streams[:3]
+    got = index_streams(streams)
+    assert len(got) == len(streams)
+    for bs, ix in zip(streams, got):
+        one = StreamIndex(bs)
+        assert (ix.n, ix.h, ix.w, ix.bitmap_len) == (one.n, one.h, one.w, one.bitmap_len)
+        for name in ("payload_off", "payload_len", "bitmap_off"):
+            assert np.array_equal(getattr(ix, name), getattr(one, name)), name
+        assert np.array_equal(ix.frame_type[:ix.n], one.frame_type[:one.n])
+
+
+def test_batch_walk_reports_first_bad_stream():
+    from paper_2602_09725_b200.codec import index_streams
+    fr = cases.codec_frames(dict(kind="jitter", n=5, h=20, w=37, gop=3, seed=9))
+    bs = ref.encode_frames(fr, 3)
+    for bad, want in ((bs[:40], _oracle_error(bs[:40])), (bs + b"\x00", _oracle_error(bs + b"\x00")),
+                      (bs[:5], _oracle_error(bs[:5]))):
+        batch = [bs, bs, bad, bs, bs[:-1]]
+        with pytest.raises(DecodeError) as ei:
+            index_streams(batch)
+        assert ei.value.frame_index == want
