@@ -407,16 +407,16 @@ def _decode_fed(datas, out, s, dev):
     # payload).  Each segment gets 128-byte lines of its own in the blob, at the
     # source's offset modulo 128 (16-byte copies; no L1 line shared with bytes
     # that land later).
-    lo_l, len_l, src_l = [], [], []
-    for j, ix in enumerate(idxs):
-        ends = (ix.payload_off + ix.payload_len).astype(np.int64)
-        lo = np.concatenate([[0], ends[:-1]]).astype(np.int64)
-        lo_l.append(lo)
-        len_l.append(ends - lo)
-        src_l.append(datas[j].data_ptr() + lo)
-    lo_a = np.concatenate(lo_l) if lo_l else np.zeros(0, np.int64)
-    len_a = np.concatenate(len_l) if len_l else np.zeros(0, np.int64)
-    src_a = np.concatenate(src_l) if src_l else np.zeros(0, np.int64)
+    n_pl = np.array([3 * ix.n for ix in idxs], np.int64)
+    p_off = np.concatenate([ix.payload_off for ix in idxs]).astype(np.int64)
+    p_len = np.concatenate([ix.payload_len for ix in idxs]).astype(np.int64)
+    ends = p_off + p_len
+    first = np.concatenate([[0], np.cumsum(n_pl)[:-1]])   # each stream's first plane
+    lo_a = np.empty_like(ends)
+    lo_a[1:] = ends[:-1]
+    lo_a[first[n_pl > 0]] = 0
+    len_a = ends - lo_a
+    src_a = np.repeat(np.array([d.data_ptr() for d in datas], np.int64), n_pl) + lo_a
     region = (len_a + 255) // 128 * 128                  # >= len + (src % 128), lines
     roff = np.concatenate([[0], np.cumsum(region)])
     blob = _scratch(s, "blob", int(roff[-1]) or 1)
@@ -440,19 +440,20 @@ def _decode_fed(datas, out, s, dev):
             if tuple(fr.shape) != (f1 - f0, 3, ix.h, ix.w):
                 raise ValueError("output frames have the wrong shape")
             frames.append(fr)
-    part = list(range(len(datas)))
-    spans = [(0, int(d.numel())) for d in datas]
-    starts = np.zeros(len(datas) + 1, np.int64)
-    rc, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, 0,
-                                         symbols.data_ptr() + sym_at, frames,
-                                         seg_map=(lo_a, dst_a))
-    segs = np.empty(len(len_a), _SEG_DTYPE)
+    # the range-decode descriptors first (plane k of stream j, frame-major):
+    # the launch goes out before the reconstruction's descriptors are built
+    K = int(n_pl.sum())
+    sid = np.repeat(np.arange(len(idxs)), n_pl)
+    loc = np.arange(K, dtype=np.int64) - first[sid]
+    rc = np.empty(K, _RC_DTYPE)
+    rc["payload"] = dst_a + (p_off - lo_a)
+    rc["len"] = p_len
+    rc["symbols"] = symbols.data_ptr() + sym_at[:-1][sid] + loc * hw16_all[sid]
+    rc["n_symbols"] = hw_all[sid]
+    segs = np.empty(K, _SEG_DTYPE)
     segs["src"], segs["dst"], segs["len"] = src_a, dst_a, len_a
-    if len(segs) != len(rc):
-        return None
-    seg_of = np.arange(len(rc), dtype=np.int32)
-    h_rc, h_planes, h_chains = (_pinned_copy(x) for x in (rc, flat, ch_arr))
-    h_segs, h_of = _pinned_copy(segs), _pinned_copy(seg_of)
+    seg_of = np.arange(K, dtype=np.int32)
+    h_rc, h_segs, h_of = _pinned_copy(rc), _pinned_copy(segs), _pinned_copy(seg_of)
     ready = _scratch(s, "fed_ready", 4 * max(len(rc), 1))
     sp = _dev.stream_ptr(s)
     st = _lib.load().kvf_rc_decode_fed(
@@ -462,6 +463,13 @@ def _decode_fed(datas, out, s, dev):
     if st == _lib.KVF_EUNSUPPORTED:
         return None
     _lib.check(st)
+    part = list(range(len(datas)))
+    spans = [(0, int(d.numel())) for d in datas]
+    starts = np.zeros(len(datas) + 1, np.int64)
+    _, flat, ch_arr = _part_descriptors(part, idxs, ranges, starts, spans, 0,
+                                        symbols.data_ptr() + sym_at, frames,
+                                        seg_map=(lo_a, dst_a))
+    h_planes, h_chains = _pinned_copy(flat), _pinned_copy(ch_arr)
     if len(ch_arr):
         _lib.call("kvf_kvfc_reconstruct", C.c_void_p(h_planes.data_ptr()),
                   C.c_void_p(h_chains.data_ptr()), len(ch_arr), sp)
