@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--res", default="R1080")
     ap.add_argument("--quick", action="store_true", help="one fed decode (for ncu)")
     ap.add_argument("--ctas", type=lambda x: [int(v) for v in x.split(",")], default=[32, 128, 512])
-    ap.add_argument("--pieces", type=lambda x: [int(v) for v in x.split(",")], default=[16384, 65536])
+    ap.add_argument("--pieces", type=lambda x: [int(v) for v in x.split(",")], default=[4096, 16384])
     ap.add_argument("--copy-only", type=lambda x: [int(v) for v in x.split(",") if v],
                     default=[32, 128, 512])
     a = ap.parse_args()

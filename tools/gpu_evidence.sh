@@ -40,9 +40,11 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:pack
     -o $O/prof_pack_stream -f python tools/pack_sweep.py --schedules single_read --steps 2 > $O/ncu_pack_stream.txt 2>&1; echo "pack_stream rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:rc_decode_kernel -s 0 -c 1 \
     -o $O/prof_rc_decode_fed -f python tools/fed_probe.py --quick > $O/ncu_fed.txt 2>&1; echo "fed rc=$?"
-FETCH="python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_decode -s 2 -c 1 \
-    -o $O/prof_rc_decode -f $FETCH > $O/ncu_rc_decode.txt 2>&1; echo "rc_decode rc=$?"
+# the plain range decoder over all of C2's planes in one launch (device-resident bytes)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:rc_decode -s 0 -c 1 \
+    -o $O/prof_rc_decode -f python tools/rc_probe.py > $O/ncu_rc_decode.txt 2>&1; echo "rc_decode rc=$?"
+timeout 600 python tools/rc_probe.py > $O/rc_probe.txt 2>&1
+timeout 600 python tools/rc_probe.py --pinned > $O/rc_probe_fed.txt 2>&1
 fi
 
 # summaries on the box (the reports themselves stay there: gpurun brings back <= 64 MiB)
