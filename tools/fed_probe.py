@@ -57,13 +57,20 @@ def main():
             run(f"fed copy_ctas={ctas} piece={piece}")
     # the copy side alone: a fed launch whose decoders have nothing to decode
     real = codec._part_descriptors
+    real_pin = codec._pinned_copy
 
     def no_decode(*x, **kw):
         rc, flat, ch = real(*x, **kw)
-        rc["len"] = 0
-        rc["n_symbols"] = 0
         return rc, flat[:0], ch[:0]
+
+    def no_symbols(a):  # the fed launch's range-decode descriptors: nothing to decode
+        if a.dtype == codec._RC_DTYPE:
+            a = a.copy()
+            a["len"] = 0
+            a["n_symbols"] = 0
+        return real_pin(a)
     codec._part_descriptors = no_decode
+    codec._pinned_copy = no_symbols
     for ctas in a.copy_only:
         codec._FED_COPY_CTAS, codec._FED_PIECE = ctas, 16384
         codec.decode_batch(streams, out=frames)
@@ -76,6 +83,7 @@ def main():
         print(f"copy only copy_ctas={ctas}: {ms:.1f} ms = {nb / ms / 1e6:.1f} GB/s (incl. walk)",
               flush=True)
     codec._part_descriptors = real
+    codec._pinned_copy = real_pin
 
 
 if __name__ == "__main__":
