@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kDecThreads)
   const uint32_t nsym = (uint32_t)st.n_symbols;
   uint32_t pack = 0;
   const bool aligned4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  const uint32_t full4 = nsym & ~3u;  // symbols in whole 4-symbol groups
   float rcp = rcp_approx(total);  // ~1/total of the symbol being decoded
   // FED: blocks of kFedBlock symbols, each started only once the next
   // kFedBlock * 8 + 16 payload bytes have landed.  A symbol takes at most 7
@@ -358,8 +359,13 @@ __global__ void __launch_bounds__(kDecThreads)
         rng <<= 8;
         bw.refill();
       }
-      pack = (pack >> 8) | (s << 24);  // 4 symbols per 32-bit store
-      if ((k & 3) == 3) {
+      pack = (pack >> 8) | (s << 24);  // 4 symbols per 32-bit word
+      if (!FED && aligned4 && k < full4) {
+        // every symbol stores its group's word (no branch on k & 3); the
+        // group's last symbol stores the complete word last.  (93.7 -> 92.3 ms
+        // on C2 R1080; the fed kernel measured slower with it: 95.4 -> 98.4)
+        *reinterpret_cast<uint32_t*>(out + (k & ~3u)) = pack;
+      } else if ((k & 3) == 3) {
         if (aligned4) {
           *reinterpret_cast<uint32_t*>(out + (k - 3)) = pack;
         } else {
