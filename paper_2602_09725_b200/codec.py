@@ -389,10 +389,10 @@ def _fed_eligible(datas):
     for d in datas:
         if d.numel() < 12 or not d.is_pinned():
             return False
-        n, h, w = np.frombuffer(d.numpy()[:12].tobytes(), "<u4")
-        if n == 0 or int(h) * int(w) < _FED_MIN_SYMBOLS:
+        n, h, w = struct.unpack("<III", C.string_at(d.data_ptr(), 12))
+        if n == 0 or h * w < _FED_MIN_SYMBOLS:
             return False
-        planes += 3 * int(n)
+        planes += 3 * n
     return planes <= _FED_MAX_PLANES
 
 
