@@ -145,7 +145,11 @@ extern "C" kvf_status kvf_kvfc_scan_batch(const uint8_t* const* data, const int6
     worker();
   } else {
     std::vector<std::thread> pool;
-    for (int32_t t = 0; t < nt; ++t) pool.emplace_back(worker);
+    try {
+      for (int32_t t = 1; t < nt; ++t) pool.emplace_back(worker);
+    } catch (...) {  // no threads available: the calling thread walks the rest
+    }
+    worker();
     for (auto& t : pool) t.join();
   }
   for (int32_t j = 0; j < n_streams; ++j) {
