@@ -212,7 +212,12 @@ __device__ void copy_pieces(const FeedArgs& F) {
   }
 }
 
-template <bool FED>
+// EVERY: every symbol stores its 4-symbol group's word (no branch on k & 3):
+// one more instruction per symbol, faster while each scheduler holds at most
+// one decoder warp (latency-bound: C2 R1080 93.7 -> 92.0 ms), slower once
+// warps share schedulers (issue-bound: C2 R240 22.1 -> 27.9 ms) and in the fed
+// kernel (95.4 -> 98.4 ms).
+template <bool FED, bool EVERY = false>
 __global__ void __launch_bounds__(kDecThreads)
     rc_decode_kernel(const kvf_rc_stream* __restrict__ streams, int n, const FeedArgs F) {
   extern __shared__ uint4 M[];  // [32 chunks][kDecThreads] x 16 B
@@ -360,10 +365,8 @@ __global__ void __launch_bounds__(kDecThreads)
         bw.refill();
       }
       pack = (pack >> 8) | (s << 24);  // 4 symbols per 32-bit word
-      if (!FED && aligned4 && k < full4) {
-        // every symbol stores its group's word (no branch on k & 3); the
-        // group's last symbol stores the complete word last.  (93.7 -> 92.3 ms
-        // on C2 R1080; the fed kernel measured slower with it: 95.4 -> 98.4)
+      if (EVERY && aligned4 && k < full4) {
+        // the group's last symbol stores the complete word last
         *reinterpret_cast<uint32_t*>(out + (k & ~3u)) = pack;
       } else if ((k & 3) == 3) {
         if (aligned4) {
@@ -624,9 +627,17 @@ extern "C" kvf_status kvf_rc_decode(const kvf_rc_stream* d_streams, int32_t n_st
   // CTAs (448 streams) are resident per SM and the grid spreads over every SM.
   const size_t smem = (size_t)kDecThreads * 256 * sizeof(uint16_t);
   const int grid = (n_streams + kDecThreads - 1) / kDecThreads;
+  int dev = 0, sms = 0;
+  KVF_CHECK_CUDA(cudaGetDevice(&dev));
+  KVF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   FeedArgs none{};
-  rc_decode_kernel<false><<<grid, kDecThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      d_streams, n_streams, none);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // few enough warps that a scheduler rarely holds two, even when a few such
+  // launches (decode_batch parts) run side by side
+  if (grid <= 2 * sms)
+    rc_decode_kernel<false, true><<<grid, kDecThreads, smem, s>>>(d_streams, n_streams, none);
+  else
+    rc_decode_kernel<false, false><<<grid, kDecThreads, smem, s>>>(d_streams, n_streams, none);
   KVF_CHECK_CUDA(cudaGetLastError());
   return KVF_OK;
 }
