@@ -396,6 +396,42 @@ def _fed_eligible(datas):
     return planes <= _FED_MAX_PLANES
 
 
+def _fed_segments(idxs, src_ptrs):
+    """Copy segments of whole streams, vectorised over all planes (stream j's
+    planes k = 3 f + p in order): plane k's bytes run from the previous
+    payload's end (0 for a stream's first plane) to the end of its payload,
+    i.e. its mode bitmap, length word and payload.  `src_ptrs[j]`: the host
+    address of stream j's first byte."""
+    n_pl = np.array([3 * ix.n for ix in idxs], np.int64)
+    p_off = np.concatenate([ix.payload_off for ix in idxs]).astype(np.int64)
+    p_len = np.concatenate([ix.payload_len for ix in idxs]).astype(np.int64)
+    ends = p_off + p_len
+    first = np.concatenate([[0], np.cumsum(n_pl)[:-1]]).astype(np.int64)
+    lo = np.empty_like(ends)
+    lo[1:] = ends[:-1]
+    lo[first[n_pl > 0]] = 0
+    return {"n_pl": n_pl, "first": first, "p_off": p_off, "p_len": p_len, "lo": lo,
+            "len": ends - lo, "src": np.repeat(np.asarray(src_ptrs, np.int64), n_pl) + lo}
+
+
+def _fed_rc(idxs, segp, dst, sym_ptr):
+    """kvf_rc_stream array of whole streams whose plane segments sit at device
+    addresses `dst` (what _part_descriptors gives with seg_map=(lo, dst));
+    `sym_ptr[j]`: stream j's symbol slots."""
+    n_pl, first = segp["n_pl"], segp["first"]
+    hw = np.array([ix.h * ix.w for ix in idxs], np.int64)
+    hw16 = -(-hw // 16) * 16
+    K = int(n_pl.sum())
+    sid = np.repeat(np.arange(len(idxs)), n_pl)
+    loc = np.arange(K, dtype=np.int64) - first[sid]
+    rc = np.empty(K, _RC_DTYPE)
+    rc["payload"] = dst + (segp["p_off"] - segp["lo"])
+    rc["len"] = segp["p_len"]
+    rc["symbols"] = np.asarray(sym_ptr, np.int64)[sid] + loc * hw16[sid]
+    rc["n_symbols"] = hw[sid]
+    return rc
+
+
 def _decode_fed(datas, out, s, dev):
     """decode_batch of whole pinned streams through one kvf_rc_decode_fed
     launch + one reconstruction launch on `s`; None if the batch does not fit
@@ -407,16 +443,8 @@ def _decode_fed(datas, out, s, dev):
     # payload).  Each segment gets 128-byte lines of its own in the blob, at the
     # source's offset modulo 128 (16-byte copies; no L1 line shared with bytes
     # that land later).
-    n_pl = np.array([3 * ix.n for ix in idxs], np.int64)
-    p_off = np.concatenate([ix.payload_off for ix in idxs]).astype(np.int64)
-    p_len = np.concatenate([ix.payload_len for ix in idxs]).astype(np.int64)
-    ends = p_off + p_len
-    first = np.concatenate([[0], np.cumsum(n_pl)[:-1]])   # each stream's first plane
-    lo_a = np.empty_like(ends)
-    lo_a[1:] = ends[:-1]
-    lo_a[first[n_pl > 0]] = 0
-    len_a = ends - lo_a
-    src_a = np.repeat(np.array([d.data_ptr() for d in datas], np.int64), n_pl) + lo_a
+    segp = _fed_segments(idxs, [d.data_ptr() for d in datas])
+    lo_a, len_a, src_a = segp["lo"], segp["len"], segp["src"]
     region = (len_a + 255) // 128 * 128                  # >= len + (src % 128), lines
     roff = np.concatenate([[0], np.cumsum(region)])
     blob = _scratch(s, "blob", int(roff[-1]) or 1)
@@ -442,14 +470,8 @@ def _decode_fed(datas, out, s, dev):
             frames.append(fr)
     # the range-decode descriptors first (plane k of stream j, frame-major):
     # the launch goes out before the reconstruction's descriptors are built
-    K = int(n_pl.sum())
-    sid = np.repeat(np.arange(len(idxs)), n_pl)
-    loc = np.arange(K, dtype=np.int64) - first[sid]
-    rc = np.empty(K, _RC_DTYPE)
-    rc["payload"] = dst_a + (p_off - lo_a)
-    rc["len"] = p_len
-    rc["symbols"] = symbols.data_ptr() + sym_at[:-1][sid] + loc * hw16_all[sid]
-    rc["n_symbols"] = hw_all[sid]
+    rc = _fed_rc(idxs, segp, dst_a, symbols.data_ptr() + sym_at)
+    K = len(rc)
     segs = np.empty(K, _SEG_DTYPE)
     segs["src"], segs["dst"], segs["len"] = src_a, dst_a, len_a
     seg_of = np.arange(K, dtype=np.int32)

@@ -110,3 +110,35 @@ def test_batch_walk_reports_first_bad_stream():
         with pytest.raises(DecodeError) as ei:
             index_streams(batch)
         assert ei.value.frame_index == want
+
+
+def test_fed_descriptors_match_part_descriptors():
+    """The fed decode's vectorised copy segments tile every stream exactly, and
+    its range-decode descriptors equal _part_descriptors' with the same
+    segment map (host-side arithmetic only: fake addresses)."""
+    import torch
+    from paper_2602_09725_b200 import codec
+    streams = [ref.encode_frames(cases.codec_frames(c), c["gop"]) for c in cases.CODEC_CASES]
+    streams = [s for s in streams if struct.unpack_from("<I", s, 0)[0] > 0][:6]
+    idxs = codec.index_streams(streams)
+    src = [(j + 1) << 24 | (j * 37 % 128) for j in range(len(streams))]
+    segp = codec._fed_segments(idxs, src)
+    at = 0
+    for j, (bs, ix) in enumerate(zip(streams, idxs)):
+        k = slice(at, at + 3 * ix.n)
+        lo, ln = segp["lo"][k], segp["len"][k]
+        assert lo[0] == 0 and lo[-1] + ln[-1] == len(bs)
+        assert np.array_equal(lo[1:], (lo + ln)[:-1])
+        assert np.array_equal(segp["src"][k], src[j] + lo)
+        at += 3 * ix.n
+    region = (segp["len"] + 255) // 128 * 128
+    dst = (1 << 40) + np.concatenate([[0], np.cumsum(region)[:-1]]) + segp["src"] % 128
+    sym_ptr = (1 << 36) + np.arange(len(streams), dtype=np.int64) * (1 << 28)
+    rc = codec._fed_rc(idxs, segp, dst, sym_ptr)
+    frames = [torch.empty((ix.n, 3, ix.h, ix.w), dtype=torch.uint8) for ix in idxs]
+    n = len(streams)
+    rc2, _, _ = codec._part_descriptors(list(range(n)), idxs, [(0, ix.n) for ix in idxs],
+                                        np.zeros(n + 1, np.int64),
+                                        [(0, len(s)) for s in streams], 0, sym_ptr, frames,
+                                        seg_map=(segp["lo"], dst))
+    assert np.array_equal(rc, rc2)
