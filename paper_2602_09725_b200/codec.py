@@ -375,7 +375,7 @@ def _decode_batch(streams, out, stream, ranges, indices, max_parts, staged):
 # after the batch's last copy.
 _FED_MIN_SYMBOLS = 98_304
 _FED_PIECE = 4 * 1024
-_FED_COPY_CTAS = 128
+_FED_COPY_CTAS = 256  # 96 or fewer starve the decoders (208 ms at 96 on C2 R1080); 128-512 all ~98.8 ms
 
 
 _FED_MAX_PLANES = 50_000  # one wave of 1-warp decoder CTAs (+ copy CTAs) on 148 SMs
