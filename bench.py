@@ -678,10 +678,10 @@ def main():
 
     fetch = None
     if not args.no_fetch:
-        fetch = fetch_to_ready(w, 3, torch)
+        fetch = fetch_to_ready(w, 7, torch)   # median of 7 wall-clock steps
         fetch["resolution"] = args.res
         if args.res != "R240":  # the class the adaptive policy picks at >= 10 Gbps
-            alt = fetch_to_ready(w, 3, torch, w.frames_at("R240"))
+            alt = fetch_to_ready(w, 7, torch, w.frames_at("R240"))
             fetch["R240"] = {k: alt[k] for k in ("ms", "coded_bytes", "decode_bitexact")}
 
     cpu = None

@@ -123,7 +123,7 @@ class StreamIndex:
         _lib.check(st)
 
 
-_SCAN_THREADS = 8  # host threads of the batched stream walk
+_SCAN_THREADS = 16  # host threads of the batched stream walk
 
 
 def index_streams(datas) -> list:
